@@ -1,0 +1,279 @@
+/*
+ * epicorr_b200.h — C ABI of the B200-native epicorr hot path.
+ *
+ * This is the drop-in boundary: every entry point replaces one reference
+ * C++ solver entry point of `epicorr` (paths below are relative to the
+ * reference tree, proj/...). Plain C types only: pointers, sizes, POD
+ * structs. No exceptions cross the ABI: every call returns an EPC_* status
+ * and, on failure, the message the reference would have thrown (its
+ * `e.what()` text) is available from epc_last_error().
+ *
+ * Memory: functions taking `int mem` accept EPC_MEM_HOST (pageable or pinned
+ * host buffers; the call copies in and out on the context stream and
+ * synchronises) or EPC_MEM_DEVICE (pointers into the context device's HBM;
+ * the call still synchronises before returning so row/scalar outputs are
+ * valid). Layouts are the reference's (proj/include/epicorr/grid.hpp:1-6,
+ * 39-44): axis 1 fastest; faces `i + n1*(j + m2*k)` with n1 = m1 + 1;
+ * cells `i + m1*(j + m2*k)`; a column (j,k) is contiguous.
+ */
+#ifndef EPICORR_B200_H
+#define EPICORR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (map onto the reference's exception types) ---------- */
+enum {
+    EPC_OK = 0,
+    EPC_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    EPC_ERR_RUNTIME = 2,          /* std::runtime_error    */
+    EPC_ERR_DOMAIN = 3,           /* std::domain_error     */
+    EPC_ERR_CUDA = 4,             /* CUDA runtime failure (no reference analogue) */
+    EPC_ERR_UNSUPPORTED = 5       /* path out of scope of this build (e.g. SGS) */
+};
+
+enum { EPC_MEM_HOST = 0, EPC_MEM_DEVICE = 1 };
+
+/* proj/include/epicorr/report.hpp:12 */
+enum { EPC_STOP_CONVERGED = 0, EPC_STOP_MAX_ITERATIONS = 1, EPC_STOP_LINE_SEARCH_FAILURE = 2,
+       EPC_STOP_ERROR = 3 };
+/* proj/include/epicorr/admm.hpp:31 */
+enum { EPC_RHO_FIXED = 0, EPC_RHO_ADAPTIVE = 1, EPC_RHO_ADAPTIVE_BOUNDED = 2 };
+/* proj/include/epicorr/gn_pcg.hpp:21 */
+enum { EPC_PRECOND_NONE = 0, EPC_PRECOND_JACOBI = 1, EPC_PRECOND_BLOCK_JACOBI = 2,
+       EPC_PRECOND_SGS = 3 };
+
+/* GridSpec, proj/include/epicorr/grid.hpp:16-52 */
+typedef struct epc_grid {
+    int dim;          /* 2 or 3 */
+    int m[3];         /* cells per axis; m[2] == 1 in 2D */
+    double h[3];      /* spacings */
+    double origin[3];
+} epc_grid;
+
+/* ObjectiveParams, proj/include/epicorr/objective.hpp:25-34 */
+typedef struct epc_objective_params {
+    double alpha; /* 50   */
+    double beta;  /* 10   */
+    double gamma; /* 1e-3 */
+    int enforce_linf_box;
+} epc_objective_params;
+
+/* ADMMConfig, proj/include/epicorr/admm.hpp:36-50 */
+typedef struct epc_admm_config {
+    double rho0, rho_min;
+    int schedule;
+    double eps_abs, eps_rel;
+    int max_iter;
+    double tau_incr, tau_decr, mu;
+    int sqp_max_iter;
+    double sqp_tol_rel;
+    int check_kkt;
+    int threads; /* accepted for API parity; the device path ignores it */
+} epc_admm_config;
+
+/* GNConfig, proj/include/epicorr/gn_pcg.hpp:26-40 */
+typedef struct epc_gn_config {
+    double eta;
+    int max_outer;
+    double eps_obj, eps_iter, eps_grad;
+    double wolfe_c1, wolfe_c2;
+    int max_pcg, max_ls;
+    int precond;
+    int threads;
+} epc_gn_config;
+
+/* AdmmIterRow, proj/include/epicorr/report.hpp:28-40 */
+typedef struct epc_admm_row {
+    int level, iter;
+    double primal_res, dual_res, eps_pri, eps_dual, rho, lagrangian, kkt_violation;
+    double b_update_s, wall_s;
+} epc_admm_row;
+
+/* GnIterRow, proj/include/epicorr/report.hpp:16-26 */
+typedef struct epc_gn_row {
+    int level, iter;
+    double j_value, grad_norm, step;
+    int pcg_iters;
+    double pcg_relres, pcg_relres_prec, wall_s;
+} epc_gn_row;
+
+/* BUpdateStats, proj/include/epicorr/admm.hpp:91-95 */
+typedef struct epc_bupdate_stats {
+    long sqp_iters, qp_iters;
+    double kkt_violation;
+    int max_active; /* largest active set met in any column QP (diagnostic) */
+} epc_bupdate_stats;
+
+/* Result of one solve: stop reason + message, SolveReport
+ * (proj/include/epicorr/report.hpp:42-51). Rows go to caller arrays. */
+typedef struct epc_solve_status {
+    int stop;
+    int nrows;
+    char message[256];
+} epc_solve_status;
+
+/* Objective values, ObjectiveEval (proj/include/epicorr/objective.hpp:84-90) */
+typedef struct epc_objective_eval {
+    double value, dist, smooth, pen;
+    int feasible;
+} epc_objective_eval;
+
+/* PcgResult scalars (proj/include/epicorr/gn_pcg.hpp:49-55) */
+typedef struct epc_pcg_result {
+    int iters;
+    double relres, relres_prec;
+    int reached_tol;
+} epc_pcg_result;
+
+/* DualUpdate scalars (proj/include/epicorr/admm.hpp:107-111) */
+typedef struct epc_dual_result {
+    double primal_res, dual_res, eps_pri, eps_dual;
+} epc_dual_result;
+
+typedef struct epc_context epc_context;
+
+/* ---- defaults matching the reference's default member initialisers ----- */
+void epc_default_params(epc_objective_params* p);     /* objective.hpp:26-31 */
+void epc_default_admm_config(epc_admm_config* c);     /* admm.hpp:37-47 */
+void epc_default_gn_config(epc_gn_config* c);         /* gn_pcg.hpp:27-37 */
+
+/* ---- context ------------------------------------------------------------
+ * One context per device; all work goes to `stream` (a cudaStream_t; NULL
+ * means a stream owned by the context). Not thread-safe per context. */
+int epc_context_create(int device, void* stream, epc_context** out);
+void epc_context_destroy(epc_context* ctx);
+int epc_set_stream(epc_context* ctx, void* stream);
+const char* epc_last_error(const epc_context* ctx);
+/* Bitmask of optional modes, EPC_MODE_*; default 0 (reference-exact). */
+int epc_set_mode(epc_context* ctx, int mode_bits);
+/* Per-kernel CUDA-event timing on the context stream (for the roofline). */
+int epc_profile_enable(epc_context* ctx, int on);
+/* Fills up to `cap` entries: name (static string), total ms, launch count. */
+int epc_profile_read(epc_context* ctx, const char** names, double* total_ms, long* launches,
+                     int cap, int* count);
+void epc_profile_reset(epc_context* ctx);
+/* Kernel launches issued on this context since creation / last reset. */
+long epc_launch_count(const epc_context* ctx);
+void epc_reset_launch_count(epc_context* ctx);
+
+/* ---- ADMM (proj/src/admm.cpp) ------------------------------------------- */
+
+/* admm_solve, proj/include/epicorr/admm.hpp:127-129, proj/src/admm.cpp:488-560.
+ * b, z, u: in = initial state (NULL = zero start, like an empty StaggeredField),
+ * out = final state (must be non-NULL to receive it). *rho: in = init.rho
+ * (<= 0 selects cfg->rho0), out = final rho. rows: capacity max_rows.
+ * Errors thrown by the reference before the loop (validate, infeasible start)
+ * return EPC_ERR_INVALID_ARGUMENT; in-loop errors give stop = EPC_STOP_ERROR
+ * with the reference's message and return EPC_OK, as the reference does. */
+int epc_admm_solve(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+                   const double* iminus, const double* b_in, const double* z_in,
+                   const double* u_in, double* b_out, double* z_out, double* u_out,
+                   double* rho, const epc_objective_params* p, const epc_admm_config* cfg,
+                   int level_tag, epc_admm_row* rows, int max_rows, epc_solve_status* status);
+
+/* Batched admm_solve over `npairs` independent volume pairs sharing one grid
+ * (C4 config). Arrays are pair-major (pair p at offset p*cells / p*faces);
+ * rho[npairs], rows[npairs*max_rows], status[npairs]. Each pair keeps its
+ * own rho schedule and stop test; results equal npairs separate calls. */
+int epc_admm_solve_batch(epc_context* ctx, const epc_grid* g, int npairs, int mem,
+                         const double* iplus, const double* iminus, const double* b_in,
+                         const double* z_in, const double* u_in, double* b_out,
+                         double* z_out, double* u_out, double* rho,
+                         const epc_objective_params* p, const epc_admm_config* cfg,
+                         int level_tag, epc_admm_row* rows, int max_rows,
+                         epc_solve_status* status);
+
+/* b_update, admm.hpp:100-102, admm.cpp:301-443 (with residual_column,
+ * qp_active_set, verify_qp_kkt, clamp_column_diffs). stats may be NULL. */
+int epc_b_update(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+                 const double* iminus, const double* b, const double* z, const double* u,
+                 double rho, const epc_objective_params* p, const epc_admm_config* cfg,
+                 double* b_out, epc_bupdate_stats* stats);
+
+/* z_update, admm.hpp:105, admm.cpp:445-451 (DctCoupledSolver::solve,
+ * operators.cpp:388-418). */
+int epc_z_update(epc_context* ctx, const epc_grid* g, int mem, const double* b, const double* u,
+                 double rho, double alpha, double* z_out);
+
+/* DctCoupledSolver::solve on an arbitrary right-hand side, operators.hpp:99. */
+int epc_dct_solve(epc_context* ctx, const epc_grid* g, int mem, const double* rhs, double alpha,
+                  double rho, double* out);
+
+/* dual_update_and_residuals, admm.hpp:113-115, admm.cpp:453-476. */
+int epc_dual_update(epc_context* ctx, const epc_grid* g, int mem, const double* b_new,
+                    const double* z_new, const double* z_old, const double* u_old, double rho,
+                    double eps_abs, double eps_rel, double* u_out, epc_dual_result* out);
+
+/* augmented_lagrangian, admm.hpp:87-89, admm.cpp:287-299. */
+int epc_augmented_lagrangian(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+                             const double* iminus, const double* b, const double* z,
+                             const double* u, double rho, double alpha, double* out);
+
+/* rho_schedule, admm.hpp:119-120, admm.cpp:478-486 (host scalar logic). */
+double epc_rho_schedule(int schedule, double rho, double rho_min, double primal_res,
+                        double dual_res, double tau_incr, double tau_decr, double mu);
+
+/* qp_active_set + verify_qp_kkt over `nqp` independent column QPs of size n
+ * (admm.hpp:74-81, admm.cpp:114-265), host memory, QP-major arrays of n
+ * (gd, go, c, x0, x) and n-1 (lambda, active_sign) per QP. status[q] is an
+ * EPC_* code; its message for the lowest failing QP is in epc_last_error.
+ * kkt[q] = verify_qp_kkt of the result (may be NULL). */
+int epc_qp_active_set_batch(epc_context* ctx, int nqp, int n, double h, const double* gd,
+                            const double* go, const double* c, const double* x0, int max_iter,
+                            double* x, double* lambda, int* active_sign, int* iters,
+                            double* kkt, int* status);
+
+/* ---- GN-PCG (proj/src/gn_pcg.cpp, proj/src/objective.cpp) ---------------- */
+
+/* gauss_newton_solve, gn_pcg.hpp:81-83, gn_pcg.cpp:197-292. */
+int epc_gn_solve(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+                 const double* iminus, const double* b0, double* b_out,
+                 const epc_objective_params* p, const epc_gn_config* cfg, int level_tag,
+                 epc_gn_row* rows, int max_rows, epc_solve_status* status);
+
+/* objective_gn, objective.hpp:93-94, objective.cpp:231-264. grad (faces) is
+ * written only when need_grad and the point is feasible; residual (cells)
+ * may be NULL. */
+int epc_objective_gn(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+                     const double* iminus, const double* b, const epc_objective_params* p,
+                     int need_grad, epc_objective_eval* out, double* grad, double* residual);
+
+/* GnHessian ctor + column_part + preconditioner_blocks (objective.cpp:266-348).
+ * diag/off: column part; pdiag: preconditioner_blocks().diag (any may be NULL). */
+int epc_gn_hessian_build(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+                         const double* iminus, const double* b, const epc_objective_params* p,
+                         double* diag, double* off, double* pdiag);
+
+/* GnHessian::apply at linearisation point b, objective.cpp:302-331. */
+int epc_gn_hessian_apply(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+                         const double* iminus, const double* b, const epc_objective_params* p,
+                         const double* x, double* y);
+
+/* make_preconditioner(kind) applied to r at linearisation point b,
+ * gn_pcg.cpp:37-90 (none / jacobi / block_jacobi; sgs -> EPC_ERR_UNSUPPORTED). */
+int epc_precond_apply(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+                      const double* iminus, const double* b, const epc_objective_params* p,
+                      int kind, const double* r, double* z);
+
+/* pcg(H(b), M_kind, grad, eta, max_iters), gn_pcg.cpp:92-131. */
+int epc_pcg(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+            const double* iminus, const double* b, const epc_objective_params* p, int kind,
+            const double* grad, double eta, int max_iters, double* d, epc_pcg_result* out);
+
+/* residual, objective.hpp:48, objective.cpp:77-91 (cells). */
+int epc_residual(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+                 const double* iminus, const double* b, double* r);
+
+/* Library build identity (arch, mode) for logs. */
+const char* epc_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EPICORR_B200_H */

@@ -1,0 +1,374 @@
+// ref_harness.cpp — TEST INFRASTRUCTURE ONLY (oracle/, never shipped).
+//
+// extern "C" adapter from oracle_api.h onto the UNMODIFIED reference library
+// compiled from /root/reference/proj/src (see oracle/Makefile). It only
+// marshals plain arrays into the reference's own types and calls its public
+// entry points; no reference arithmetic is restated here.
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "epicorr/admm.hpp"
+#include "epicorr/gn_pcg.hpp"
+#include "epicorr/grid.hpp"
+#include "epicorr/image.hpp"
+#include "epicorr/objective.hpp"
+#include "epicorr/operators.hpp"
+
+#include "oracle_api.h"
+
+using namespace epicorr;
+
+namespace {
+
+int g_threads = 1;
+
+GridSpec to_grid(const epc_grid* g) {
+    GridSpec s;
+    s.dim = g->dim;
+    for (int a = 0; a < 3; ++a) {
+        s.m[a] = g->m[a];
+        s.h[a] = g->h[a];
+        s.origin[a] = g->origin[a];
+    }
+    s.validate();
+    return s;
+}
+
+StaggeredField faces(const GridSpec& g, const double* v) {
+    StaggeredField f(g);
+    if (v) std::memcpy(f.v.data(), v, sizeof(double) * f.v.size());
+    return f;
+}
+
+ImageVolume cells(const GridSpec& g, const double* v) {
+    ImageVolume f(g);
+    std::memcpy(f.v.data(), v, sizeof(double) * f.v.size());
+    return f;
+}
+
+ObjectiveParams to_params(const epc_objective_params* p) {
+    ObjectiveParams o;
+    o.alpha = p->alpha;
+    o.beta = p->beta;
+    o.gamma = p->gamma;
+    o.enforce_linf_box = p->enforce_linf_box != 0;
+    return o;
+}
+
+ADMMConfig to_admm(const epc_admm_config* c) {
+    ADMMConfig o;
+    o.rho0 = c->rho0;
+    o.rho_min = c->rho_min;
+    o.schedule = RhoSchedule(c->schedule);
+    o.eps_abs = c->eps_abs;
+    o.eps_rel = c->eps_rel;
+    o.max_iter = c->max_iter;
+    o.tau_incr = c->tau_incr;
+    o.tau_decr = c->tau_decr;
+    o.mu = c->mu;
+    o.sqp_max_iter = c->sqp_max_iter;
+    o.sqp_tol_rel = c->sqp_tol_rel;
+    o.check_kkt = c->check_kkt != 0;
+    o.threads = c->threads > 0 ? c->threads : g_threads;
+    return o;
+}
+
+GNConfig to_gn(const epc_gn_config* c) {
+    GNConfig o;
+    o.eta = c->eta;
+    o.max_outer = c->max_outer;
+    o.eps_obj = c->eps_obj;
+    o.eps_iter = c->eps_iter;
+    o.eps_grad = c->eps_grad;
+    o.wolfe_c1 = c->wolfe_c1;
+    o.wolfe_c2 = c->wolfe_c2;
+    o.max_pcg = c->max_pcg;
+    o.max_ls = c->max_ls;
+    o.precond = PrecondKind(c->precond);
+    o.threads = c->threads > 0 ? c->threads : g_threads;
+    return o;
+}
+
+void put_msg(char* msg, size_t len, const char* text) {
+    if (!msg || len == 0) return;
+    std::snprintf(msg, len, "%s", text);
+}
+
+template <class F>
+int guarded(char* msg, size_t len, F&& f) {
+    put_msg(msg, len, "");
+    try {
+        f();
+        return EPC_OK;
+    } catch (const std::invalid_argument& e) {
+        put_msg(msg, len, e.what());
+        return EPC_ERR_INVALID_ARGUMENT;
+    } catch (const std::domain_error& e) {
+        put_msg(msg, len, e.what());
+        return EPC_ERR_DOMAIN;
+    } catch (const std::exception& e) {
+        put_msg(msg, len, e.what());
+        return EPC_ERR_RUNTIME;
+    }
+}
+
+void copy_out(const StaggeredField& f, double* out) {
+    if (out) std::memcpy(out, f.v.data(), sizeof(double) * f.v.size());
+}
+
+} // namespace
+
+extern "C" {
+
+void oracle_set_threads(int threads) { g_threads = threads > 0 ? threads : 1; }
+
+int oracle_admm_solve(const epc_grid* gg, const double* iplus, const double* iminus,
+                      const double* b_in, const double* z_in, const double* u_in,
+                      double* b_out, double* z_out, double* u_out, double* rho,
+                      const epc_objective_params* p, const epc_admm_config* cfg, int level_tag,
+                      epc_admm_row* rows, int max_rows, epc_solve_status* status) {
+    char* msg = status ? status->message : nullptr;
+    return guarded(msg, status ? sizeof status->message : 0, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        ADMMState init;
+        if (b_in) init.b = faces(g, b_in);
+        if (z_in) init.z = faces(g, z_in);
+        if (u_in) init.u = faces(g, u_in);
+        init.rho = rho ? *rho : 0.0;
+        AdmmSolveResult res = admm_solve(pair, std::move(init), to_params(p), to_admm(cfg), level_tag);
+        copy_out(res.state.b, b_out);
+        copy_out(res.state.z, z_out);
+        copy_out(res.state.u, u_out);
+        if (rho) *rho = res.state.rho;
+        const int n = int(std::min<std::size_t>(res.report.admm.size(), std::size_t(max_rows)));
+        for (int i = 0; i < n; ++i) {
+            const AdmmIterRow& r = res.report.admm[i];
+            rows[i] = epc_admm_row{r.level,    r.iter,       r.primal_res, r.dual_res,
+                                   r.eps_pri,  r.eps_dual,   r.rho,        r.lagrangian,
+                                   r.kkt_violation, r.b_update_s, r.wall_s};
+        }
+        if (status) {
+            status->stop = int(res.report.stop);
+            status->nrows = int(res.report.admm.size());
+            std::snprintf(status->message, sizeof status->message, "%s", res.report.message.c_str());
+        }
+    });
+}
+
+int oracle_gn_solve(const epc_grid* gg, const double* iplus, const double* iminus,
+                    const double* b0, double* b_out, const epc_objective_params* p,
+                    const epc_gn_config* cfg, int level_tag, epc_gn_row* rows, int max_rows,
+                    epc_solve_status* status) {
+    char* msg = status ? status->message : nullptr;
+    return guarded(msg, status ? sizeof status->message : 0, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        GnSolveResult res =
+            gauss_newton_solve(pair, faces(g, b0), to_params(p), to_gn(cfg), level_tag);
+        copy_out(res.b, b_out);
+        const int n = int(std::min<std::size_t>(res.report.gn.size(), std::size_t(max_rows)));
+        for (int i = 0; i < n; ++i) {
+            const GnIterRow& r = res.report.gn[i];
+            rows[i] = epc_gn_row{r.level,     r.iter,       r.j_value,        r.grad_norm, r.step,
+                                 r.pcg_iters, r.pcg_relres, r.pcg_relres_prec, r.wall_s};
+        }
+        if (status) {
+            status->stop = int(res.report.stop);
+            status->nrows = int(res.report.gn.size());
+            std::snprintf(status->message, sizeof status->message, "%s", res.report.message.c_str());
+        }
+    });
+}
+
+int oracle_b_update(const epc_grid* gg, const double* iplus, const double* iminus,
+                    const double* b, const double* z, const double* u, double rho,
+                    const epc_objective_params* p, const epc_admm_config* cfg, double* b_out,
+                    epc_bupdate_stats* stats, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        ADMMState st;
+        st.b = faces(g, b);
+        st.z = faces(g, z);
+        st.u = faces(g, u);
+        st.rho = rho;
+        BUpdateStats s;
+        StaggeredField out = b_update(pair, st, to_params(p), to_admm(cfg), &s);
+        copy_out(out, b_out);
+        if (stats) {
+            stats->sqp_iters = s.sqp_iters;
+            stats->qp_iters = s.qp_iters;
+            stats->kkt_violation = s.kkt_violation;
+            stats->max_active = -1;
+        }
+    });
+}
+
+int oracle_z_update(const epc_grid* gg, const double* b, const double* u, double rho,
+                    double alpha, double* z_out, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        ADMMState st;
+        st.b = faces(g, b);
+        st.u = faces(g, u);
+        st.rho = rho;
+        const DctCoupledSolver dct(g, g_threads);
+        copy_out(z_update(st, alpha, dct), z_out);
+    });
+}
+
+int oracle_dct_solve(const epc_grid* gg, const double* rhs, double alpha, double rho,
+                     double* out, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        const DctCoupledSolver dct(g, g_threads);
+        copy_out(dct.solve(faces(g, rhs), alpha, rho), out);
+    });
+}
+
+int oracle_dual_update(const epc_grid* gg, const double* b_new, const double* z_new,
+                       const double* z_old, const double* u_old, double rho, double eps_abs,
+                       double eps_rel, double* u_out, epc_dual_result* out) {
+    return guarded(nullptr, 0, [&] {
+        const GridSpec g = to_grid(gg);
+        DualUpdate du = dual_update_and_residuals(faces(g, b_new), faces(g, z_new),
+                                                  faces(g, z_old), faces(g, u_old), rho,
+                                                  eps_abs, eps_rel);
+        copy_out(du.u, u_out);
+        if (out) *out = epc_dual_result{du.primal_res, du.dual_res, du.eps_pri, du.eps_dual};
+    });
+}
+
+double oracle_augmented_lagrangian(const epc_grid* gg, const double* iplus, const double* iminus,
+                                   const double* b, const double* z, const double* u,
+                                   double rho, double alpha) {
+    const GridSpec g = to_grid(gg);
+    const VolumePair pair(cells(g, iplus), cells(g, iminus));
+    return augmented_lagrangian(pair, faces(g, b), faces(g, z), faces(g, u), rho, alpha,
+                                g_threads);
+}
+
+int oracle_qp_active_set(int n, double h, const double* gd, const double* go, const double* c,
+                         const double* x0, int max_iter, double* x, double* lambda,
+                         int* active_sign, int* iters, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        QpResult r = qp_active_set(n, h, std::span<const double>(gd, n),
+                                   std::span<const double>(go, n), std::span<const double>(c, n),
+                                   std::span<const double>(x0, n), max_iter);
+        std::memcpy(x, r.x.data(), sizeof(double) * n);
+        std::memcpy(lambda, r.lambda.data(), sizeof(double) * (n - 1));
+        std::memcpy(active_sign, r.active_sign.data(), sizeof(int) * (n - 1));
+        if (iters) *iters = r.iters;
+    });
+}
+
+double oracle_verify_qp_kkt(int n, double h, const double* gd, const double* go,
+                            const double* c, const double* x, const double* lambda,
+                            const int* active_sign) {
+    QpResult r;
+    r.x.assign(x, x + n);
+    r.lambda.assign(lambda, lambda + (n - 1));
+    r.active_sign.assign(active_sign, active_sign + (n - 1));
+    return verify_qp_kkt(n, h, std::span<const double>(gd, n), std::span<const double>(go, n),
+                         std::span<const double>(c, n), r);
+}
+
+int oracle_objective_gn(const epc_grid* gg, const double* iplus, const double* iminus,
+                        const double* b, const epc_objective_params* p, int need_grad,
+                        epc_objective_eval* out, double* grad, double* residual) {
+    return guarded(nullptr, 0, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        ObjectiveEval ev = objective_gn(pair, faces(g, b), to_params(p), g_threads, need_grad != 0);
+        if (out) *out = epc_objective_eval{ev.value, ev.dist, ev.smooth, ev.pen, ev.feasible ? 1 : 0};
+        if (grad && !ev.grad.v.empty()) copy_out(ev.grad, grad);
+        if (residual && !ev.residual.v.empty())
+            std::memcpy(residual, ev.residual.v.data(), sizeof(double) * ev.residual.v.size());
+    });
+}
+
+int oracle_gn_hessian_build(const epc_grid* gg, const double* iplus, const double* iminus,
+                            const double* b, const epc_objective_params* p, double* diag,
+                            double* off, double* pdiag, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        GnHessian h(pair, faces(g, b), to_params(p), g_threads);
+        const std::size_t n = std::size_t(g.faces());
+        if (diag) std::memcpy(diag, h.column_part().diag.data(), sizeof(double) * n);
+        if (off) std::memcpy(off, h.column_part().off.data(), sizeof(double) * n);
+        if (pdiag) {
+            TridiagBlocks t = h.preconditioner_blocks();
+            std::memcpy(pdiag, t.diag.data(), sizeof(double) * n);
+        }
+    });
+}
+
+int oracle_gn_hessian_apply(const epc_grid* gg, const double* iplus, const double* iminus,
+                            const double* b, const epc_objective_params* p, const double* x,
+                            double* y, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        GnHessian h(pair, faces(g, b), to_params(p), g_threads);
+        copy_out(h.apply(faces(g, x)), y);
+    });
+}
+
+int oracle_precond_apply(const epc_grid* gg, const double* iplus, const double* iminus,
+                         const double* b, const epc_objective_params* p, int kind,
+                         const double* r, double* z, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        GnHessian h(pair, faces(g, b), to_params(p), g_threads);
+        LinOp m = make_preconditioner(PrecondKind(kind), h, g_threads);
+        std::vector<double> rv(r, r + g.faces()), zv;
+        m(rv, zv);
+        std::memcpy(z, zv.data(), sizeof(double) * zv.size());
+    });
+}
+
+int oracle_pcg(const epc_grid* gg, const double* iplus, const double* iminus, const double* b,
+               const epc_objective_params* p, int kind, const double* grad, double eta,
+               int max_iters, double* d, epc_pcg_result* out, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        GnHessian h(pair, faces(g, b), to_params(p), g_threads);
+        LinOp m = make_preconditioner(PrecondKind(kind), h, g_threads);
+        LinOp apply_h = [&h](const std::vector<double>& x, std::vector<double>& y) {
+            y.resize(x.size());
+            h.apply(x, y);
+        };
+        std::vector<double> gv(grad, grad + g.faces());
+        PcgResult res = pcg(apply_h, m, gv, eta, max_iters);
+        std::memcpy(d, res.d.data(), sizeof(double) * res.d.size());
+        if (out) *out = epc_pcg_result{res.iters, res.relres, res.relres_prec, res.reached_tol ? 1 : 0};
+    });
+}
+
+int oracle_residual(const epc_grid* gg, const double* iplus, const double* iminus,
+                    const double* b, double* r) {
+    return guarded(nullptr, 0, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        CellField rr = residual(pair, faces(g, b), g_threads);
+        std::memcpy(r, rr.v.data(), sizeof(double) * rr.v.size());
+    });
+}
+
+double oracle_rho_schedule(int schedule, double rho, double rho_min, double primal_res,
+                           double dual_res, double tau_incr, double tau_decr, double mu) {
+    return rho_schedule(RhoSchedule(schedule), rho, rho_min, primal_res, dual_res, tau_incr,
+                        tau_decr, mu);
+}
+
+} // extern "C"
