@@ -1,0 +1,333 @@
+#!/usr/bin/env python3
+"""bench.py — ADMM time-to-solution and voxel-iterations/s on B200.
+
+Workload (BASELINE.json configs[2], the config its metric is quoted on):
+ADMM on the 256x256x96 synthetic volume pair, fp64, 100 outer iterations
+from b = 0, reference-default alpha/rho schedule, eps_abs = eps_rel = 1e-300
+so the iteration count is fixed. One "step" = one full solve.
+
+  value  = faces x ADMM iterations x ranks / max-over-ranks device time,
+           inputs resident in HBM (EPC_MEM_DEVICE through the C ABI);
+  e2e    = the same through the C ABI with pinned host buffers: every step
+           copies I+/I- in and b/z/u out inside the timed region.
+
+Multi-GPU (torchrun, one process per GPU): ADMM does not shard a single
+C3 volume (BASELINE runs C3 on 1 GPU), so each rank solves its own volume
+pair (independent replicas, weak scaling, no data-path collective); the
+barrier + max-over-ranks timing uses NCCL only for the timing plumbing.
+
+--impl reference: the reference's own CPU implementation of this path
+(oracle/_ref: proj/src compiled unmodified) on all host threads, same config
+and metric, each step a bounded sample (a few ADMM iterations) of the solve.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_1607_00531_b200 import abi, synth  # noqa: E402
+
+METRIC = "voxel-iterations/s (ADMM, 256x256x96, fp64)"
+UNIT = "face-iterations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--iters", type=int, default=None, help="ADMM iterations per solve")
+    ap.add_argument("--scale", type=float, default=1.0, help="intensity scale (x400 variant)")
+    ap.add_argument("--ref-iters", type=int, default=2, help="ADMM iterations per reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+DEFAULT_ITERS = {"C1": 50, "C2": 50, "C3": 100, "C4": 50, "C5": 50}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def dist_setup(n):
+    if n <= 1 and "RANK" not in os.environ:
+        return 0, 1, 0, None
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", n))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29511")
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    return rank, world, local, dist
+
+
+def cpu_reference(d, iters, threads):
+    """Reference CPU implementation (oracle/_ref) if built, else the C port."""
+    from oracle import ffi
+    kind = "reference" if os.path.exists(ffi.PATHS["ref"]) else "port"
+    chk = ffi.load("ref" if kind == "reference" else "oracle")
+    if kind == "reference":
+        chk.set_threads(threads)
+    cfg = abi.AdmmConfig(max_iter=iters, eps_abs=1e-300, eps_rel=1e-300,
+                         threads=threads if kind == "reference" else 1)
+    t = time.perf_counter()
+    chk.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
+    dt = time.perf_counter() - t
+    return kind, dt, (threads if kind == "reference" else 1)
+
+
+def run_reference_arm(a, iters):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return 0
+    d = synth.make_config(a.config, scale=a.scale)
+    threads = os.cpu_count() or 1
+    times = []
+    kind = cores = None
+    for s in range(a.warmup + a.steps):
+        kind, dt, cores = cpu_reference(d, a.ref_iters, threads)
+        if s >= a.warmup:
+            times.append(dt)
+    t = float(np.mean(times))
+    value = d.grid.faces * a.ref_iters / t
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"ADMM {a.config} {'x'.join(map(str, d.grid.dims()))}",
+                       "iterations_per_step": a.ref_iters, "full_solve_iterations": iters,
+                       "intensity_scale": a.scale},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": f"{a.ref_iters} ADMM iterations of the {a.config} solve per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    a = parse()
+    iters = a.iters or DEFAULT_ITERS.get(a.config, 50)
+    if a.impl == "reference":
+        return run_reference_arm(a, iters)
+
+    import torch
+    rank, world, local, dist = dist_setup(a.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1607_00531_b200.epicorr import Context
+    stream = torch.cuda.Stream(device=dev)
+    ctx = Context(local, stream=stream)
+
+    # each rank: its own volume pair (replica) of the config
+    spec = synth.CONFIGS[a.config]
+    from dataclasses import replace
+    spec = replace(spec, scale=a.scale, seed=spec.seed + 1000 * rank)
+    d = synth.make_pair(spec)
+    g = d.grid
+    ip_d = torch.from_numpy(d.iplus).to(dev)
+    im_d = torch.from_numpy(d.iminus).to(dev)
+    ip_h = torch.from_numpy(d.iplus).pin_memory()
+    im_h = torch.from_numpy(d.iminus).pin_memory()
+    bo_h = torch.empty(g.faces, dtype=torch.float64).pin_memory()
+    zo_h = torch.empty(g.faces, dtype=torch.float64).pin_memory()
+    uo_h = torch.empty(g.faces, dtype=torch.float64).pin_memory()
+    cfg = abi.AdmmConfig(max_iter=iters, eps_abs=1e-300, eps_rel=1e-300)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def solve_device():
+        return ctx.admm_solve(g, ip_d, im_d, cfg=cfg)
+
+    def solve_host():
+        # C ABI with pinned host buffers: H2D of I+/I-, D2H of b, z, u inside the call
+        import ctypes as C
+        rows = (abi.AdmmRow * iters)()
+        st = abi.SolveStatus()
+        rho = C.c_double(0.0)
+        P = lambda t: C.c_void_p(t.data_ptr())
+        rc = ctx.lib.epc_admm_solve(ctx.h, C.byref(g), abi.EPC_MEM_HOST, P(ip_h), P(im_h), None,
+                                    None, None, P(bo_h), P(zo_h), P(uo_h), C.byref(rho),
+                                    C.byref(abi.ObjectiveParams()), C.byref(cfg), 0, rows, iters,
+                                    C.byref(st))
+        assert rc == 0, ctx._err()
+        return st
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def timed(fn, k):
+        """Device time of k steps (CUDA events on the launching stream),
+        L2 flushed (256 MB write) before each step outside the events."""
+        tot = 0.0
+        launches = 0
+        for _ in range(k):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            ctx.reset_launch_count()
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            launches += ctx.launch_count()
+            tot += e0.elapsed_time(e1) / 1e3
+        return tot, launches
+
+    for _ in range(a.warmup):
+        solve_device()
+    barrier()
+    with ClockSampler(local) as clk:
+        barrier()
+        t_dev, launches = timed(solve_device, a.steps)
+        barrier()
+    t_max = t_dev
+    if dist is not None:
+        tt = torch.tensor([t_dev], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    faces_iters = g.faces * iters
+    value = faces_iters * world * a.steps / t_max
+
+    # e2e through the C ABI with pinned host buffers
+    solve_host()
+    barrier()
+    t_e2e, _ = timed(solve_host, a.steps)
+    if dist is not None:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e = faces_iters * world * a.steps / t_e2e
+
+    # roofline: per-kernel CUDA-event timing of one profiled solve
+    ctx.profile(True)
+    ctx.profile_reset()
+    solve_device()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    nf, nc = g.faces, g.cells
+    # algorithmic bytes per launch: b-step reads I+,I-,b,z,u and
+    # writes b; each DCT GEMM reads + writes one face field (rhs GEMM reads b,u).
+    alg = {"admm_bstep": 8 * (2 * nc + 4 * nf), "dct_fwd2": 8 * 3 * nf, "dct_fwd3_div": 8 * 2 * nf,
+           "dct_inv3": 8 * 2 * nf, "dct_inv2_dual": 8 * 7 * nf}
+    kernels = []
+    for name, (ms, n) in prof.items():
+        if name in alg and n:
+            per = ms / n / 1e3
+            gbs = alg[name] / per / 1e9
+            kernels.append({"kernel": name, "ms_per_launch": ms / n, "alg_bytes": alg[name],
+                            "achieved_gbs": gbs, "frac_hbm": gbs / hbm_peak})
+    top = max(prof.items(), key=lambda kv: kv[1][0])
+    bname, (bms, bn) = top
+    b_per = bms / bn / 1e3
+    b_ach = alg.get(bname, 0) / b_per / 1e9
+    roofline = {"bound": "hbm", "kernel": bname, "achieved": b_ach, "peak": hbm_peak,
+                "peak_source": peak_src, "unit": "GB/s", "frac": b_ach / hbm_peak,
+                "traffic": None, "share_of_step": bms / sum(v[0] for v in prof.values()),
+                "note": "b-step is fp64-latency bound (serial SQP/QP chains), not HBM bound",
+                "kernels": kernels}
+
+    cpu = None
+    if rank == 0 and not a.no_cpu_baseline:
+        try:
+            kind, dt, cores = cpu_reference(d, a.ref_iters, os.cpu_count() or 1)
+            cpu = {"value": g.faces * a.ref_iters / dt, "unit": UNIT, "cores": cores, "kind": kind,
+                   "sample": f"{a.ref_iters} ADMM iterations of the {a.config} solve"}
+        except Exception as e:  # the checker is optional on a bench box
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
+                   "sample": str(e)[:120]}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_max / a.steps * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"ADMM {a.config} {'x'.join(map(str, g.dims()))}, "
+                                       f"{iters} iterations, fp64, from b=0",
+                           "faces": g.faces, "iterations": iters, "intensity_scale": a.scale,
+                           "parallelism": f"replicas x{world}",
+                           "l2": "256 MB flush write before every timed step; working set > L2",
+                           "time_to_solution_s": t_max / a.steps},
+                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * nc * 8,
+                        "d2h_bytes_per_step": 3 * nf * 8},
+                "gpu_launches": launches, "clocks": clk.summary(),
+                "roofline": roofline, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -487,6 +487,11 @@ static int admm_validate(const epc_admm_config* c, char* msg, size_t len) {
     return EPC_OK;
 }
 
+/* Optional per-column work counters (diagnostics for kernel design; not part
+ * of the restated algorithm): [col*4 + {sqp, qp, ls_trials, max_active}]. */
+static int* g_colstats = NULL;
+void oracle_debug_colstats(int* buf) { g_colstats = buf; }
+
 /* b_update, admm.cpp:301-443 (single-threaded: columns in index order, the
  * first failing column aborts with its message, as parallel_for's chunk 0). */
 static int b_update_impl(const G* g, const double* iplus, const double* iminus, const double* b,
@@ -527,7 +532,10 @@ static int b_update_impl(const G* g, const double* iplus, const double* iminus, 
         }
         double col_kkt = 0.0;
         double s0 = -1.0;
+        int* cs = g_colstats ? g_colstats + 4 * c : NULL;
+        if (cs) cs[0] = cs[1] = cs[2] = cs[3] = 0;
         for (int sqp = 0; sqp < C->sqp_max_iter; ++sqp) {
+            if (cs) cs[0]++;
             residual_column(&ip, &im, g, x, r, jlo, jhi);
             for (int i = 0; i < n1; ++i) {
                 grad[i] = rho_w * (x[i] - tgt[i]);
@@ -568,6 +576,7 @@ static int b_update_impl(const G* g, const double* iplus, const double* iminus, 
                 break;
             }
             qp_total += qit;
+            if (cs) { cs[1] += qit; if (max_active > cs[3]) cs[3] = max_active; }
             sqp_total += 1;
             if (C->check_kkt)
                 col_kkt = dmax(col_kkt, kkt_check(n1, h1, gd, go, cqp, qx, qlam, qsign, kkts));
@@ -588,6 +597,7 @@ static int b_update_impl(const G* g, const double* iplus, const double* iminus, 
             double tls = 1.0; /* backtracking, admm.cpp:414-427 */
             int accepted = 0;
             for (int ls = 0; ls < 40; ++ls) {
+                if (cs) cs[2]++;
                 for (int i = 0; i < n1; ++i) xtrial[i] = x[i] + tls * (qx[i] - x[i]);
                 /* subproblem_value, admm.cpp:335-351 */
                 residual_column(&ip, &im, g, xtrial, rtrial, NULL, NULL);

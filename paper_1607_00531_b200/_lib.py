@@ -1,0 +1,111 @@
+"""Loader for libepicorr_b200.so (the product). No fallback: if the CUDA
+library cannot be built or loaded, every call raises."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .abi import (AdmmConfig, AdmmRow, BUpdateStats, DualResult, GnConfig, GnRow, Grid,
+                  ObjectiveEval, ObjectiveParams, PcgResult, SolveStatus, dptr, iptr)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libepicorr_b200.so")
+_lock = threading.Lock()
+_lib = None
+
+# every symbol include/epicorr_b200.h declares
+EXPORTS = [
+    "epc_default_params", "epc_default_admm_config", "epc_default_gn_config",
+    "epc_context_create", "epc_context_destroy", "epc_set_stream", "epc_last_error",
+    "epc_set_mode", "epc_profile_enable", "epc_profile_read", "epc_profile_reset",
+    "epc_launch_count", "epc_reset_launch_count", "epc_admm_solve", "epc_admm_solve_batch",
+    "epc_b_update", "epc_z_update", "epc_dct_solve", "epc_dual_update",
+    "epc_augmented_lagrangian", "epc_rho_schedule", "epc_qp_active_set_batch", "epc_gn_solve",
+    "epc_objective_gn", "epc_gn_hessian_build", "epc_gn_hessian_apply", "epc_precond_apply",
+    "epc_pcg", "epc_residual", "epc_build_info", "epc_bstep_timing",
+]
+
+
+class _Tolerant:
+    """Declares argtypes only for symbols present (the ABI test checks that
+    all of EXPORTS are)."""
+
+    def __init__(self, lib):
+        self.__dict__["_l"] = lib
+
+    def __getattr__(self, name):
+        try:
+            return getattr(self._l, name)
+        except AttributeError:
+            return C.CFUNCTYPE(None)()  # dummy sink for argtypes
+
+
+def _declare(L):
+    L = _Tolerant(L)
+    G, P = C.POINTER(Grid), C.POINTER(ObjectiveParams)
+    A, N = C.POINTER(AdmmConfig), C.POINTER(GnConfig)
+    X = C.c_void_p
+    L.epc_context_create.argtypes = [C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
+    L.epc_context_destroy.argtypes = [X]
+    L.epc_context_destroy.restype = None
+    L.epc_set_stream.argtypes = [X, C.c_void_p]
+    L.epc_last_error.argtypes = [X]
+    L.epc_last_error.restype = C.c_char_p
+    L.epc_set_mode.argtypes = [X, C.c_int]
+    L.epc_profile_enable.argtypes = [X, C.c_int]
+    L.epc_profile_read.argtypes = [X, C.POINTER(C.c_char_p), dptr, C.POINTER(C.c_long), C.c_int,
+                                   C.POINTER(C.c_int)]
+    L.epc_profile_reset.argtypes = [X]
+    L.epc_profile_reset.restype = None
+    L.epc_launch_count.argtypes = [X]
+    L.epc_launch_count.restype = C.c_long
+    L.epc_reset_launch_count.argtypes = [X]
+    L.epc_reset_launch_count.restype = None
+    L.epc_admm_solve.argtypes = [X, G, C.c_int, X, X, X, X, X, X, X, X, dptr, P, A, C.c_int,
+                                 C.POINTER(AdmmRow), C.c_int, C.POINTER(SolveStatus)]
+    L.epc_admm_solve_batch.argtypes = [X, G, C.c_int, C.c_int, X, X, X, X, X, X, X, X, dptr, P, A,
+                                       C.c_int, C.POINTER(AdmmRow), C.c_int, C.POINTER(SolveStatus)]
+    L.epc_b_update.argtypes = [X, G, C.c_int, X, X, X, X, X, C.c_double, P, A, X,
+                               C.POINTER(BUpdateStats)]
+    L.epc_z_update.argtypes = [X, G, C.c_int, X, X, C.c_double, C.c_double, X]
+    L.epc_dct_solve.argtypes = [X, G, C.c_int, X, C.c_double, C.c_double, X]
+    L.epc_dual_update.argtypes = [X, G, C.c_int, X, X, X, X, C.c_double, C.c_double, C.c_double, X,
+                                  C.POINTER(DualResult)]
+    L.epc_augmented_lagrangian.argtypes = [X, G, C.c_int, X, X, X, X, X, C.c_double, C.c_double, dptr]
+    L.epc_rho_schedule.argtypes = [C.c_int] + [C.c_double] * 7
+    L.epc_rho_schedule.restype = C.c_double
+    L.epc_qp_active_set_batch.argtypes = [X, C.c_int, C.c_int, C.c_double, X, X, X, X, C.c_int, X,
+                                          X, X, X, X, X]
+    L.epc_gn_solve.argtypes = [X, G, C.c_int, X, X, X, X, P, N, C.c_int, C.POINTER(GnRow), C.c_int,
+                               C.POINTER(SolveStatus)]
+    L.epc_objective_gn.argtypes = [X, G, C.c_int, X, X, X, P, C.c_int, C.POINTER(ObjectiveEval), X, X]
+    L.epc_gn_hessian_build.argtypes = [X, G, C.c_int, X, X, X, P, X, X, X]
+    L.epc_gn_hessian_apply.argtypes = [X, G, C.c_int, X, X, X, P, X, X]
+    L.epc_precond_apply.argtypes = [X, G, C.c_int, X, X, X, P, C.c_int, X, X]
+    L.epc_pcg.argtypes = [X, G, C.c_int, X, X, X, P, C.c_int, X, C.c_double, C.c_int, X,
+                          C.POINTER(PcgResult)]
+    L.epc_residual.argtypes = [X, G, C.c_int, X, X, X, X]
+    L.epc_build_info.restype = C.c_char_p
+    L.epc_bstep_timing.argtypes = [X, C.POINTER(C.c_longlong)]
+
+
+def load(build_if_missing=True):
+    """Load (building in-tree first if missing or stale) the CUDA library."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if build_if_missing:
+            from . import build as _build
+            try:
+                _build.build()
+            except Exception:
+                if not os.path.exists(LIB_PATH):
+                    raise
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libepicorr_b200.so not found at {LIB_PATH}; run build()")
+        L = C.CDLL(LIB_PATH)
+        _declare(L)
+        _lib = L
+        return L

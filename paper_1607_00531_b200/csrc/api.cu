@@ -1,0 +1,1162 @@
+// api.cu — C ABI (include/epicorr_b200.h) and the host driver of the ADMM
+// loop. The loop restates admm_solve (proj/src/admm.cpp:488-560) with every
+// per-iteration pass on the device: b-step (bstep.cu), z-step + dual update
+// (zstep.cu), then one small device->host read of the per-pair scalars that
+// the reference's row / stop test / rho schedule need.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+struct EpcError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& m) { throw EpcError{code, m}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(EPC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(x) ck((x), #x)
+
+template <class F>
+int guarded(epc_context* ctx, F&& f) {
+    try {
+        if (ctx) ctx->last_error.clear();
+        f();
+        return EPC_OK;
+    } catch (const EpcError& e) {
+        if (ctx) ctx->last_error = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->last_error = e.what();
+        return EPC_ERR_RUNTIME;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// grid
+// ---------------------------------------------------------------------------
+struct Geo {
+    int dim, m1, m2, m3, n1;
+    long long ncell, nface, ncol;
+    double h1, h2, h3, o1, V;
+};
+
+// GridSpec::validate, proj/src/grid.cpp:33-47
+Geo make_geo(const epc_grid* g) {
+    if (!g) fail(EPC_ERR_INVALID_ARGUMENT, "null grid");
+    if (g->dim != 2 && g->dim != 3) fail(EPC_ERR_INVALID_ARGUMENT, "GridSpec: dim must be 2 or 3");
+    if (g->m[0] < 2 || g->m[1] < 2) fail(EPC_ERR_INVALID_ARGUMENT, "GridSpec: m1 and m2 must be >= 2");
+    if (g->dim == 3 && g->m[2] < 2) fail(EPC_ERR_INVALID_ARGUMENT, "GridSpec: m3 must be >= 2 in 3D");
+    if (g->dim == 2 && g->m[2] != 1) fail(EPC_ERR_INVALID_ARGUMENT, "GridSpec: m3 must be 1 in 2D");
+    for (int a = 0; a < 3; ++a) {
+        if (!(g->h[a] > 0.0) || !std::isfinite(g->h[a]))
+            fail(EPC_ERR_INVALID_ARGUMENT, "GridSpec: spacings must be positive");
+        if (!std::isfinite(g->origin[a])) fail(EPC_ERR_INVALID_ARGUMENT, "GridSpec: origin must be finite");
+    }
+    if (g->m[0] + 1 > 32767) fail(EPC_ERR_UNSUPPORTED, "m1 too large for the column kernel");
+    Geo o;
+    o.dim = g->dim;
+    o.m1 = g->m[0];
+    o.m2 = g->m[1];
+    o.m3 = g->m[2];
+    o.n1 = o.m1 + 1;
+    o.ncell = (long long)o.m1 * o.m2 * o.m3;
+    o.nface = (long long)o.n1 * o.m2 * o.m3;
+    o.ncol = (long long)o.m2 * o.m3;
+    o.h1 = g->h[0];
+    o.h2 = g->h[1];
+    o.h3 = g->h[2];
+    o.o1 = g->origin[0];
+    o.V = g->h[0] * g->h[1] * g->h[2];  // cell_volume, grid.hpp:35
+    return o;
+}
+
+// ---------------------------------------------------------------------------
+// device scratch slots
+// ---------------------------------------------------------------------------
+enum Slot {
+    S_IP, S_IM, S_B0, S_B1, S_Z0, S_Z1, S_U0, S_U1, S_H1, S_H2,
+    S_COLI, S_COLD, S_QBUF, S_SBUF, S_PART, S_PART2, S_SCAL, S_PAIR, S_MATS, S_CNT,
+    S_TMP0, S_TMP1, S_TMP2, S_TMP3,
+    S_GN0, S_GN1, S_GN2, S_GN3, S_GN4, S_GN5, S_GN6, S_GN7, S_GN8, S_GN9,
+    S_COUNT
+};
+
+void* slot(epc_context* ctx, int s, size_t bytes) {
+    if ((int)ctx->bufs.size() < S_COUNT) ctx->bufs.resize(S_COUNT);
+    DevBuf& b = ctx->bufs[s];
+    if (b.bytes < bytes) {
+        if (b.ptr) {
+            CK(cudaStreamSynchronize(ctx->stream));
+            CK(cudaFree(b.ptr));
+            b.ptr = nullptr;
+            b.bytes = 0;
+        }
+        const size_t want = std::max<size_t>(bytes, 256);
+        CK(cudaMalloc(&b.ptr, want));
+        b.bytes = want;
+    }
+    return b.ptr;
+}
+
+template <class T>
+T* slot_t(epc_context* ctx, int s, size_t count) {
+    return static_cast<T*>(slot(ctx, s, count * sizeof(T)));
+}
+
+void* pinned(epc_context* ctx, size_t bytes) {
+    if (ctx->pinned_bytes < bytes) {
+        if (ctx->pinned) CK(cudaFreeHost(ctx->pinned));
+        ctx->pinned = nullptr;
+        CK(cudaMallocHost(&ctx->pinned, std::max<size_t>(bytes, 4096)));
+        ctx->pinned_bytes = std::max<size_t>(bytes, 4096);
+    }
+    return ctx->pinned;
+}
+
+void h2d(epc_context* ctx, void* dst, const void* src, size_t bytes) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+}
+void d2h(epc_context* ctx, void* dst, const void* src, size_t bytes) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+}
+void d2d(epc_context* ctx, void* dst, const void* src, size_t bytes) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+}
+void sync(epc_context* ctx) { CK(cudaStreamSynchronize(ctx->stream)); }
+
+// Stage an input array into slot `s` (copy, never alias: the reference takes
+// its inputs by const& / by value). nullptr -> zeros.
+double* stage_in(epc_context* ctx, int s, int mem, const double* src, size_t count) {
+    double* d = slot_t<double>(ctx, s, count);
+    if (!src) CK(cudaMemsetAsync(d, 0, count * sizeof(double), ctx->stream));
+    else if (mem == EPC_MEM_HOST) h2d(ctx, d, src, count * sizeof(double));
+    else d2d(ctx, d, src, count * sizeof(double));
+    return d;
+}
+
+void stage_out(epc_context* ctx, int mem, double* dst, const double* src, size_t count) {
+    if (!dst) return;
+    if (mem == EPC_MEM_HOST) d2h(ctx, dst, src, count * sizeof(double));
+    else d2d(ctx, dst, src, count * sizeof(double));
+}
+
+void check_launch() { ck(cudaGetLastError(), "kernel launch"); }
+
+int grid1d(epc_context* ctx, long long n, int block = 256) {
+    long long b = (n + block - 1) / block;
+    return (int)std::max<long long>(1, std::min<long long>(b, (long long)ctx->num_sms * 16));
+}
+
+// ---------------------------------------------------------------------------
+// DCT operator matrices, built on the host with the reference's formulas
+// (dct2_matrix, operators.cpp:287-295; neumann_eigenvalues, :275-282) so the
+// device uses the very same coefficients.
+// ---------------------------------------------------------------------------
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+std::vector<double> dct2_matrix(int m) {
+    std::vector<double> c((size_t)m * m);
+    const double s0 = std::sqrt(1.0 / m), sq = std::sqrt(2.0 / m);
+    for (int q = 0; q < m; ++q)
+        for (int j = 0; j < m; ++j)
+            c[(size_t)q * m + j] = (q == 0 ? s0 : sq) * std::cos(kPi * q * (2.0 * j + 1.0) / (2.0 * m));
+    return c;
+}
+
+std::vector<double> neumann_eigenvalues(int m, double h) {
+    std::vector<double> lam(m);
+    for (int q = 0; q < m; ++q) {
+        const double s = std::sin(kPi * q / (2.0 * m));
+        lam[q] = 4.0 / (h * h) * s * s;
+    }
+    return lam;
+}
+
+struct DctMats {
+    const double *c2, *c2t, *c3, *c3t, *lam23;
+};
+
+DctMats upload_dct(epc_context* ctx, const Geo& g) {
+    const int m2 = g.m2, m3 = g.m3;
+    std::vector<double> c2 = dct2_matrix(m2), c3 = m3 > 1 ? dct2_matrix(m3) : std::vector<double>(1, 1.0);
+    for (double v : c2)
+        if (v == 0.0) fail(EPC_ERR_UNSUPPORTED, "DCT matrix has an exact zero coefficient");
+    for (double v : c3)
+        if (v == 0.0) fail(EPC_ERR_UNSUPPORTED, "DCT matrix has an exact zero coefficient");
+    const int k3 = m3 > 1 ? m3 : 1;
+    std::vector<double> c2t((size_t)m2 * m2), c3t((size_t)k3 * k3);
+    for (int a = 0; a < m2; ++a)
+        for (int b = 0; b < m2; ++b) c2t[(size_t)a * m2 + b] = c2[(size_t)b * m2 + a];
+    for (int a = 0; a < k3; ++a)
+        for (int b = 0; b < k3; ++b) c3t[(size_t)a * k3 + b] = c3[(size_t)b * k3 + a];
+    std::vector<double> l2 = neumann_eigenvalues(m2, g.h2);
+    std::vector<double> l3 = m3 > 1 ? neumann_eigenvalues(m3, g.h3) : std::vector<double>{0.0};
+    std::vector<double> lam23((size_t)m2 * m3);
+    for (int k = 0; k < m3; ++k)
+        for (int j = 0; j < m2; ++j) lam23[(size_t)k * m2 + j] = l2[j] + l3[k];
+    const size_t n2 = (size_t)m2 * m2, n3 = (size_t)k3 * k3, nl = lam23.size();
+    std::vector<double> all;
+    all.reserve(2 * n2 + 2 * n3 + nl);
+    all.insert(all.end(), c2.begin(), c2.end());
+    all.insert(all.end(), c2t.begin(), c2t.end());
+    all.insert(all.end(), c3.begin(), c3.end());
+    all.insert(all.end(), c3t.begin(), c3t.end());
+    all.insert(all.end(), lam23.begin(), lam23.end());
+    double* d = slot_t<double>(ctx, S_MATS, all.size());
+    h2d(ctx, d, all.data(), all.size() * sizeof(double));
+    sync(ctx);  // `all` is pageable and goes out of scope
+    return DctMats{d, d + n2, d + 2 * n2, d + 2 * n2 + n3, d + 2 * n2 + 2 * n3};
+}
+
+// ---------------------------------------------------------------------------
+// z-step: rhs -> DCT2 -> DCT3 -> divide -> iDCT3 -> iDCT2 (+ dual epilogue)
+// ---------------------------------------------------------------------------
+struct ZArgs {
+    const double *b, *u, *z_old;  // rhs = rho V (b + u)
+    double *z_new, *u_new;        // u_new: dual update target (EPI_DUAL) or null
+    const double* rho;            // device [npairs]
+    const int* active;
+    double alpha;
+    double* partials;  // dual partials [npairs][nblk][6]
+    int nblk;          // out: blocks per pair of the dual GEMM
+    bool rhs_is_raw;   // true: b holds the rhs itself (dct_solve), u unused
+};
+
+void run_zstep(epc_context* ctx, const Geo& g, int npairs, const DctMats& M, ZArgs& a) {
+    const long long nf = g.nface;
+    double* h1 = slot_t<double>(ctx, S_H1, (size_t)nf * npairs);
+    double* h2 = slot_t<double>(ctx, S_H2, (size_t)nf * npairs);
+    GemmParams p{};
+    p.V = g.V;
+    p.rho = a.rho;
+    p.nface = nf;
+    p.lam23 = M.lam23;
+    p.alpha = a.alpha;
+    p.m2 = g.m2;
+    p.n1 = g.n1;
+    p.m3 = g.m3;
+    p.active = a.active;
+    p.zstride = nf;
+    // axis-2 operand layout: k = j, col = (k3, i)
+    auto axis2 = [&](GemmParams& q) {
+        q.M = q.K = g.m2;
+        q.N = (long long)g.m3 * g.n1;
+        q.kstride = g.n1;
+        q.cdiv = g.n1;
+        q.cstride = (long long)g.m2 * g.n1;
+    };
+    auto axis3 = [&](GemmParams& q) {
+        q.M = q.K = g.m3;
+        q.N = (long long)g.n1 * g.m2;
+        q.kstride = (long long)g.n1 * g.m2;
+        q.cdiv = q.N;
+        q.cstride = 0;
+    };
+    const int pro = a.rhs_is_raw ? PRO_PLAIN : PRO_RHS;
+    if (g.m3 > 1) {
+        GemmParams f2 = p;
+        axis2(f2);
+        f2.A = M.c2;
+        f2.in0 = a.b;
+        f2.in1 = a.u;
+        f2.out = h1;
+        launch_dct_gemm(ctx, "dct_fwd2", f2, pro, EPI_STORE, npairs, nullptr);
+        GemmParams f3 = p;
+        axis3(f3);
+        f3.A = M.c3;
+        f3.in0 = h1;
+        f3.out = h2;
+        f3.div_axis = 3;
+        launch_dct_gemm(ctx, "dct_fwd3_div", f3, PRO_PLAIN, EPI_DIVIDE, npairs, nullptr);
+        GemmParams i3 = p;
+        axis3(i3);
+        i3.A = M.c3t;
+        i3.in0 = h2;
+        i3.out = h1;
+        launch_dct_gemm(ctx, "dct_inv3", i3, PRO_PLAIN, EPI_STORE, npairs, nullptr);
+    } else {
+        GemmParams f2 = p;
+        axis2(f2);
+        f2.A = M.c2;
+        f2.in0 = a.b;
+        f2.in1 = a.u;
+        f2.out = h1;
+        f2.div_axis = 2;
+        launch_dct_gemm(ctx, "dct_fwd2_div", f2, pro, EPI_DIVIDE, npairs, nullptr);
+    }
+    GemmParams i2 = p;
+    axis2(i2);
+    i2.A = M.c2t;
+    i2.in0 = h1;
+    i2.out = a.z_new;
+    if (a.u_new) {
+        i2.bvec = a.b;
+        i2.u_old = a.u;
+        i2.z_old = a.z_old;
+        i2.u_new = a.u_new;
+        // partial buffer sized on the fly
+        const long long nblk = ((i2.N + 63) / 64) * ((i2.M + 63) / 64);
+        a.partials = slot_t<double>(ctx, S_PART, (size_t)nblk * npairs * 6);
+        i2.partials = a.partials;
+        launch_dct_gemm(ctx, "dct_inv2_dual", i2, PRO_PLAIN, EPI_DUAL, npairs, &a.nblk);
+    } else {
+        launch_dct_gemm(ctx, "dct_inv2", i2, PRO_PLAIN, EPI_STORE, npairs, &a.nblk);
+    }
+    check_launch();
+}
+
+// ---------------------------------------------------------------------------
+// b-step launch
+// ---------------------------------------------------------------------------
+struct BStepRun {
+    int* col_i;     // err, sqp, qp, maxact (4 x total)
+    double* col_d;  // kkt, fr, fd (3 x total)
+};
+
+BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip, const double* im,
+                   const double* b, const double* z, const double* u, double* b_out,
+                   const double* rho_dev, const int* active_dev, double alpha,
+                   const epc_admm_config* cfg) {
+    const long long total = g.ncol * npairs;
+    const size_t smem = bstep_smem_bytes(g.n1);
+    if (smem > ctx->smem_optin) fail(EPC_ERR_UNSUPPORTED, "column too long for shared memory");
+    CK(cudaFuncSetAttribute(k_admm_bstep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)ctx->smem_optin));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_admm_bstep, 32, smem));
+    if (per_sm < 1) fail(EPC_ERR_UNSUPPORTED, "b-step kernel does not fit on an SM");
+    const long long slots = std::min<long long>((long long)ctx->num_sms * per_sm, total);
+    const int qcap = g.m1;
+    double* qbuf = slot_t<double>(ctx, S_QBUF, (size_t)slots * qcap * g.n1);
+    double* sbuf = slot_t<double>(ctx, S_SBUF, (size_t)slots * qcap * qcap);
+    int* col_i = slot_t<int>(ctx, S_COLI, (size_t)total * 4);
+    double* col_d = slot_t<double>(ctx, S_COLD, (size_t)total * 3);
+    unsigned long long* cnt = slot_t<unsigned long long>(ctx, S_CNT, 1);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), ctx->stream));
+    BStepParams P{};
+    P.m1 = g.m1;
+    P.n1 = g.n1;
+    P.ncol = g.ncol;
+    P.ncell = g.ncell;
+    P.nface = g.nface;
+    P.dh = make_hdiv(g.h1);
+    P.o1 = g.o1;
+    P.V = g.V;
+    P.alpha = alpha;
+    P.ip = ip;
+    P.im = im;
+    P.b = b;
+    P.z = z;
+    P.u = u;
+    P.b_out = b_out;
+    P.rho = rho_dev;
+    P.active = active_dev;
+    P.sqp_max_iter = cfg->sqp_max_iter;
+    P.sqp_tol_rel = cfg->sqp_tol_rel;
+    P.check_kkt = cfg->check_kkt;
+    P.qp_cap = 6 * g.n1 + 10;  // admm.cpp:314
+    P.col_err = col_i;
+    P.col_sqp = col_i + total;
+    P.col_qp = col_i + 2 * total;
+    P.col_maxact = col_i + 3 * total;
+    P.col_kkt = col_d;
+    P.col_fr = col_d + total;
+    P.col_fd = col_d + 2 * total;
+    P.qbuf = qbuf;
+    P.sbuf = sbuf;
+    P.qcap = qcap;
+    P.counter = cnt;
+    P.total_cols = total;
+    P.timing = (ctx->mode & EPC_MODE_BSTEP_TIMING) ? slot_t<long long>(ctx, S_GN9, 16) : nullptr;
+    EPC_LAUNCH(ctx, "admm_bstep", k_admm_bstep, (unsigned)slots, 32, smem, P);
+    check_launch();
+    return BStepRun{col_i, col_d};
+}
+
+// ---------------------------------------------------------------------------
+// validation (objective.cpp:11-15, admm.cpp:28-37)
+// ---------------------------------------------------------------------------
+void validate_params(const epc_objective_params* p) {
+    if (!p) fail(EPC_ERR_INVALID_ARGUMENT, "null params");
+    if (!(p->alpha > 0.0)) fail(EPC_ERR_INVALID_ARGUMENT, "ObjectiveParams: alpha must be > 0");
+    if (!(p->beta >= 0.0)) fail(EPC_ERR_INVALID_ARGUMENT, "ObjectiveParams: beta must be >= 0");
+    if (!(p->gamma >= 0.0)) fail(EPC_ERR_INVALID_ARGUMENT, "ObjectiveParams: gamma must be >= 0");
+}
+
+void validate_admm(const epc_admm_config* c) {
+    if (!c) fail(EPC_ERR_INVALID_ARGUMENT, "null config");
+    if (!(c->rho_min > 0.0) || !(c->rho0 >= c->rho_min))
+        fail(EPC_ERR_INVALID_ARGUMENT, "ADMMConfig: need rho0 >= rho_min > 0");
+    if (!(c->eps_abs > 0.0) || !(c->eps_rel > 0.0))
+        fail(EPC_ERR_INVALID_ARGUMENT, "ADMMConfig: tolerances must be positive");
+    if (c->max_iter < 1 || c->sqp_max_iter < 1)
+        fail(EPC_ERR_INVALID_ARGUMENT, "ADMMConfig: iteration caps must be >= 1");
+    if (!(c->tau_incr > 1.0) || !(c->tau_decr > 1.0) || !(c->mu > 1.0))
+        fail(EPC_ERR_INVALID_ARGUMENT, "ADMMConfig: adaptation constants must exceed 1");
+}
+
+const char* qp_what(int code) {
+    switch (code) {
+        case 1: return "column factor: nonpositive pivot";
+        case 2: return "qp_active_set: infeasible starting point";
+        case 3: return "qp_active_set: singular Schur complement";
+        case 4: return "qp_active_set: iteration cap reached (cycling guard)";
+    }
+    return "unknown column failure";
+}
+
+// max |D1 b| > 1 test of admm_solve (admm.cpp:501-502), on the device
+__global__ void k_d1_max(const double* b, long long ncell, int m1, int n1, double h1,
+                         double* out) {
+    __shared__ double sh[8];
+    const double ih = 1.0 / h1;
+    double m = 0.0;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ncell;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long c = e / m1;
+        const int i = (int)(e - c * m1);
+        const double d = fabs((b[c * n1 + i + 1] - b[c * n1 + i]) * ih);
+        m = (m < d) ? d : m;
+    }
+    m = warp_max(m);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = (t < sh[i]) ? sh[i] : t;
+        out[blockIdx.x] = t;
+    }
+}
+
+double d1_norm_inf(epc_context* ctx, const Geo& g, const double* b_dev, int npairs, int pair) {
+    const int nb = 64;
+    double* part = slot_t<double>(ctx, S_TMP3, nb);
+    EPC_LAUNCH(ctx, "d1_max", k_d1_max, nb, 256, 0, b_dev + (size_t)pair * g.nface, g.ncell,
+               g.m1, g.n1, g.h1, part);
+    check_launch();
+    double* h = static_cast<double*>(pinned(ctx, nb * sizeof(double)));
+    d2h(ctx, h, part, nb * sizeof(double));
+    sync(ctx);
+    double m = 0.0;
+    for (int i = 0; i < nb; ++i) m = std::max(m, h[i]);
+    (void)npairs;
+    return m;
+}
+
+double rho_schedule(int schedule, double rho, double rho_min, double pr, double du, double ti,
+                    double td, double mu) {
+    if (schedule == EPC_RHO_FIXED) return rho;
+    double next = rho;
+    if (pr > mu * du) next = rho * ti;
+    else if (du > mu * pr) next = rho / td;
+    if (schedule == EPC_RHO_ADAPTIVE_BOUNDED) next = std::max(next, rho_min);
+    return next;
+}
+
+// ---------------------------------------------------------------------------
+// ADMM solve over npairs pairs sharing a grid (admm.cpp:488-560)
+// ---------------------------------------------------------------------------
+int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, const double* iplus,
+                    const double* iminus, const double* b_in, const double* z_in,
+                    const double* u_in, double* b_out, double* z_out, double* u_out,
+                    double* rho_io, const epc_objective_params* p, const epc_admm_config* cfg,
+                    int level_tag, epc_admm_row* rows, int max_rows, epc_solve_status* status) {
+    return guarded(ctx, [&] {
+        for (int q = 0; q < npairs; ++q) {
+            status[q].stop = EPC_STOP_MAX_ITERATIONS;
+            status[q].nrows = 0;
+            status[q].message[0] = 0;
+        }
+        auto pre_fail = [&](int code, const std::string& m) {
+            for (int q = 0; q < npairs; ++q) std::snprintf(status[q].message, sizeof status[q].message, "%s", m.c_str());
+            fail(code, m);
+        };
+        try {
+            validate_params(p);
+            validate_admm(cfg);
+        } catch (const EpcError& e) {
+            pre_fail(e.code, e.msg);
+        }
+        const Geo g = make_geo(gg);
+        const size_t nf = (size_t)g.nface * npairs, nc = (size_t)g.ncell * npairs;
+        const auto t0 = std::chrono::steady_clock::now();
+        // inputs (cells) and state (faces); device pointers may be used in place
+        const double* ip;
+        const double* im;
+        if (mem == EPC_MEM_DEVICE) {
+            ip = iplus;
+            im = iminus;
+        } else {
+            double* a = slot_t<double>(ctx, S_IP, nc);
+            double* b = slot_t<double>(ctx, S_IM, nc);
+            h2d(ctx, a, iplus, nc * sizeof(double));
+            h2d(ctx, b, iminus, nc * sizeof(double));
+            ip = a;
+            im = b;
+        }
+        double* B[2] = {stage_in(ctx, S_B0, mem, b_in, nf), slot_t<double>(ctx, S_B1, nf)};
+        double* Z[2] = {stage_in(ctx, S_Z0, mem, z_in, nf), slot_t<double>(ctx, S_Z1, nf)};
+        double* U[2] = {stage_in(ctx, S_U0, mem, u_in, nf), slot_t<double>(ctx, S_U1, nf)};
+        for (int q = 0; q < npairs; ++q)
+            if (b_in && d1_norm_inf(ctx, g, B[0], npairs, q) > 1.0)
+                pre_fail(EPC_ERR_INVALID_ARGUMENT, "admm_solve: infeasible starting field");
+        const DctMats M = upload_dct(ctx, g);
+
+        // per-pair device scalars: rho[npairs], active[npairs], factor[npairs]
+        char* pr = static_cast<char*>(slot(ctx, S_PAIR, (size_t)npairs * 32));
+        double* rho_dev = reinterpret_cast<double*>(pr);
+        double* fac_dev = rho_dev + npairs;
+        int* act_dev = reinterpret_cast<int*>(fac_dev + npairs);
+        std::vector<double> rho(npairs), fac(npairs, 1.0);
+        std::vector<int> active(npairs, 1), restore(npairs, 0);
+        for (int q = 0; q < npairs; ++q) rho[q] = rho_io[q] > 0.0 ? rho_io[q] : cfg->rho0;
+        // host staging block: rho, factor, active
+        const size_t scal_bytes = (size_t)npairs * (18 * 8 + 8) + 64;
+        char* hp = static_cast<char*>(pinned(ctx, scal_bytes + (size_t)npairs * 32));
+        auto push_pairs = [&]() {
+            double* hr = reinterpret_cast<double*>(hp + scal_bytes);
+            std::memcpy(hr, rho.data(), npairs * sizeof(double));
+            std::memcpy(hr + npairs, fac.data(), npairs * sizeof(double));
+            std::memcpy(reinterpret_cast<int*>(hr + 2 * npairs), active.data(), npairs * sizeof(int));
+            h2d(ctx, pr, hr, (size_t)npairs * (16 + 4));
+        };
+        push_pairs();
+        int* mask_dev = slot_t<int>(ctx, S_TMP2, npairs);
+        double* scal_d = slot_t<double>(ctx, S_SCAL, (size_t)npairs * (4 + 8));
+        long long* scal_i = slot_t<long long>(ctx, S_TMP1, (size_t)npairs * 6);
+        cudaEvent_t eb0 = epc_event_get(ctx), eb1 = epc_event_get(ctx);
+        const double V = g.V;
+        const double sqrt_n = std::sqrt((double)g.nface);
+        int n_active = npairs;
+        const bool batch = npairs > 1;
+
+        for (int it = 1; it <= cfg->max_iter && n_active > 0; ++it) {
+            // ---- b-step ----------------------------------------------------------
+            CK(cudaEventRecord(eb0, ctx->stream));
+            BStepRun br = run_bstep(ctx, g, npairs, ip, im, B[0], Z[0], U[0], B[1], rho_dev,
+                                    batch ? act_dev : nullptr, p->alpha, cfg);
+            CK(cudaEventRecord(eb1, ctx->stream));
+            const long long total = g.ncol * npairs;
+            EPC_LAUNCH(ctx, "reduce_columns", k_reduce_columns, npairs, 256, 0, br.col_i,
+                       br.col_i + total, br.col_i + 2 * total, br.col_i + 3 * total, br.col_d,
+                       br.col_d + total, br.col_d + 2 * total, g.ncol,
+                       batch ? act_dev : nullptr, scal_d, scal_i);
+            // ---- z-step + dual update ---------------------------------------------
+            ZArgs za{};
+            za.b = B[1];
+            za.u = U[0];
+            za.z_old = Z[0];
+            za.z_new = Z[1];
+            za.u_new = U[1];
+            za.rho = rho_dev;
+            za.active = batch ? act_dev : nullptr;
+            za.alpha = p->alpha;
+            run_zstep(ctx, g, npairs, M, za);
+            const int nbz = 64;
+            double* zp = slot_t<double>(ctx, S_PART2, (size_t)npairs * nbz * 2);
+            EPC_LAUNCH(ctx, "zdiff_sums", k_zdiff_sums, dim3(nbz, npairs), 256, 0, Z[1], g.nface,
+                       g.n1, g.m2, g.m3, 1.0 / g.h2, 1.0 / g.h3, zp);
+            double* sd2 = scal_d + (size_t)npairs * 4;  // 6 dual sums + 2 zdiff sums per pair
+            EPC_LAUNCH(ctx, "reduce_dual", k_reduce_partials, npairs, 256, 0, za.partials, za.nblk,
+                       6, 6, sd2);
+            EPC_LAUNCH(ctx, "reduce_zdiff", k_reduce_partials, npairs, 256, 0, zp, nbz, 2, 2,
+                       sd2 + (size_t)npairs * 6);
+            check_launch();
+            // ---- one read-back of all per-pair scalars -----------------------------
+            double* hs = reinterpret_cast<double*>(hp);
+            d2h(ctx, hs, scal_d, (size_t)npairs * 12 * sizeof(double));
+            long long* hi = reinterpret_cast<long long*>(hs + (size_t)npairs * 12);
+            d2h(ctx, hi, scal_i, (size_t)npairs * 6 * sizeof(long long));
+            sync(ctx);
+            float bms = 0.f;
+            CK(cudaEventElapsedTime(&bms, eb0, eb1));
+            const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+
+            bool any_restore = false, any_rho = false;
+            std::vector<int> was_active = active;
+            for (int q = 0; q < npairs; ++q) {
+                fac[q] = 1.0;
+                restore[q] = 0;
+                if (!was_active[q]) continue;
+                const double* cd = hs + (size_t)q * 4;
+                const long long* ci = hi + (size_t)q * 6;
+                const double* du = hs + (size_t)npairs * 4 + (size_t)q * 6;
+                const double* zd = hs + (size_t)npairs * 10 + (size_t)q * 2;
+                if (ci[0] >= 0) {  // a column failed: stop = error, state unchanged
+                    status[q].stop = EPC_STOP_ERROR;
+                    std::snprintf(status[q].message, sizeof status[q].message,
+                                  "b_update: column %lld: %s", ci[0], qp_what((int)ci[1]));
+                    active[q] = 0;
+                    restore[q] = 1;
+                    any_restore = true;
+                    --n_active;
+                    continue;
+                }
+                epc_admm_row row{};
+                row.level = level_tag;
+                row.iter = it;
+                row.rho = rho[q];
+                row.kkt_violation = cd[0];
+                row.b_update_s = bms * 1e-3;
+                // dual_update_and_residuals (admm.cpp:470-474)
+                row.primal_res = std::sqrt(du[0]);
+                row.dual_res = rho[q] * V * std::sqrt(du[1]);
+                row.eps_pri = sqrt_n * cfg->eps_abs + cfg->eps_rel * std::max(std::sqrt(du[2]), std::sqrt(du[3]));
+                row.eps_dual = sqrt_n * cfg->eps_abs + cfg->eps_rel * rho[q] * V * std::sqrt(du[4]);
+                // augmented_lagrangian (admm.cpp:267-299)
+                const double fval = 0.5 * V * cd[1] + 0.5 * p->alpha * V * cd[2];
+                double gs = zd[0];
+                if (g.dim == 3) gs += zd[1];
+                const double gval = 0.5 * p->alpha * V * gs;
+                row.lagrangian = fval + gval + rho[q] * V * du[5] + 0.5 * rho[q] * V * du[0];
+                row.wall_s = wall;
+                if (status[q].nrows < max_rows) rows[(size_t)q * max_rows + status[q].nrows] = row;
+                status[q].nrows++;
+                if (row.primal_res <= row.eps_pri && row.dual_res <= row.eps_dual) {
+                    status[q].stop = EPC_STOP_CONVERGED;
+                    active[q] = 0;
+                    --n_active;
+                    continue;
+                }
+                const double next = rho_schedule(cfg->schedule, rho[q], cfg->rho_min, row.primal_res,
+                                                 row.dual_res, cfg->tau_incr, cfg->tau_decr, cfg->mu);
+                if (next != rho[q]) {
+                    fac[q] = rho[q] / next;
+                    rho[q] = next;
+                    any_rho = true;
+                }
+            }
+            // inactive-before pairs: b-step skipped them, carry b over
+            bool any_inactive_before = false;
+            for (int q = 0; q < npairs; ++q) any_inactive_before |= !was_active[q];
+            if (any_inactive_before) {
+                std::vector<int> m(npairs);
+                for (int q = 0; q < npairs; ++q) m[q] = !was_active[q];
+                int* hm = reinterpret_cast<int*>(hi + (size_t)npairs * 6);
+                std::memcpy(hm, m.data(), npairs * sizeof(int));
+                h2d(ctx, mask_dev, hm, npairs * sizeof(int));
+                EPC_LAUNCH(ctx, "carry_b", k_copy_masked, grid1d(ctx, (long long)nf), 256, 0, B[0], B[1],
+                           g.nface, npairs, mask_dev);
+                sync(ctx);
+            }
+            if (any_restore) {  // errored pairs: keep the state from before this iteration
+                int* hm = reinterpret_cast<int*>(hi + (size_t)npairs * 6);
+                std::memcpy(hm, restore.data(), npairs * sizeof(int));
+                h2d(ctx, mask_dev, hm, npairs * sizeof(int));
+                EPC_LAUNCH(ctx, "restore_b", k_copy_masked, grid1d(ctx, (long long)nf), 256, 0, B[0], B[1], g.nface, npairs, mask_dev);
+                EPC_LAUNCH(ctx, "restore_z", k_copy_masked, grid1d(ctx, (long long)nf), 256, 0, Z[0], Z[1], g.nface, npairs, mask_dev);
+                EPC_LAUNCH(ctx, "restore_u", k_copy_masked, grid1d(ctx, (long long)nf), 256, 0, U[0], U[1], g.nface, npairs, mask_dev);
+                sync(ctx);
+            }
+            std::swap(B[0], B[1]);
+            std::swap(Z[0], Z[1]);
+            std::swap(U[0], U[1]);
+            if (any_rho) {
+                push_pairs();
+                EPC_LAUNCH(ctx, "scale_u", k_scale_pairs, grid1d(ctx, (long long)nf), 256, 0, U[0],
+                           g.nface, npairs, fac_dev);
+                check_launch();
+                for (int q = 0; q < npairs; ++q) fac[q] = 1.0;
+            } else if (n_active < npairs) {
+                push_pairs();
+            }
+            sync(ctx);
+        }
+        // outputs
+        stage_out(ctx, mem, b_out, B[0], nf);
+        stage_out(ctx, mem, z_out, Z[0], nf);
+        stage_out(ctx, mem, u_out, U[0], nf);
+        sync(ctx);
+        for (int q = 0; q < npairs; ++q) rho_io[q] = rho[q];
+        CK(cudaEventDestroy(eb0));
+        CK(cudaEventDestroy(eb1));
+    });
+}
+
+}  // namespace
+
+// ===========================================================================
+// profiling hooks (declared in common.cuh)
+// ===========================================================================
+cudaEvent_t epc_event_get(epc_context* ctx) {
+    cudaEvent_t e;
+    if (!ctx->event_pool.empty()) {
+        e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        return e;
+    }
+    cudaEventCreate(&e);
+    return e;
+}
+
+void epc_prof_begin(epc_context* ctx, const char* name, cudaEvent_t* ev0) {
+    (void)name;
+    *ev0 = epc_event_get(ctx);
+    cudaEventRecord(*ev0, ctx->stream);
+}
+
+void epc_prof_end(epc_context* ctx, const char* name, cudaEvent_t ev0) {
+    cudaEvent_t e1 = epc_event_get(ctx);
+    cudaEventRecord(e1, ctx->stream);
+    ctx->prof_pending.push_back(ProfEntry{name, ev0, e1});
+}
+
+static void prof_drain(epc_context* ctx) {
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& pe : ctx->prof_pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pe.start, pe.stop);
+        bool found = false;
+        for (auto& a : ctx->prof_acc)
+            if (std::strcmp(a.name, pe.name) == 0) {
+                a.ms += ms;
+                a.n += 1;
+                found = true;
+                break;
+            }
+        if (!found) ctx->prof_acc.push_back({pe.name, (double)ms, 1});
+        ctx->event_pool.push_back(pe.start);
+        ctx->event_pool.push_back(pe.stop);
+    }
+    ctx->prof_pending.clear();
+}
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+void epc_default_params(epc_objective_params* p) {
+    p->alpha = 50.0;
+    p->beta = 10.0;
+    p->gamma = 1e-3;
+    p->enforce_linf_box = 0;
+}
+
+void epc_default_admm_config(epc_admm_config* c) {
+    c->rho0 = 1e6;
+    c->rho_min = 1e2;
+    c->schedule = EPC_RHO_ADAPTIVE_BOUNDED;
+    c->eps_abs = 0.2;
+    c->eps_rel = 0.2;
+    c->max_iter = 50;
+    c->tau_incr = 2.0;
+    c->tau_decr = 2.0;
+    c->mu = 10.0;
+    c->sqp_max_iter = 20;
+    c->sqp_tol_rel = 1e-2;
+    c->check_kkt = 1;
+    c->threads = 1;
+}
+
+void epc_default_gn_config(epc_gn_config* c) {
+    c->eta = 0.1;
+    c->max_outer = 10;
+    c->eps_obj = 1e-3;
+    c->eps_iter = 1e-2;
+    c->eps_grad = 1e-2;
+    c->wolfe_c1 = 1e-4;
+    c->wolfe_c2 = 0.9;
+    c->max_pcg = 100;
+    c->max_ls = 30;
+    c->precond = EPC_PRECOND_BLOCK_JACOBI;
+    c->threads = 1;
+}
+
+int epc_context_create(int device, void* stream, epc_context** out) {
+    if (!out) return EPC_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    epc_context* ctx = new epc_context();
+    const int rc = guarded(ctx, [&] {
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        if (n <= 0) fail(EPC_ERR_CUDA, "no CUDA device");
+        CK(cudaSetDevice(device));
+        ctx->device = device;
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) fail(EPC_ERR_UNSUPPORTED, std::string("libepicorr_b200 is built for sm_100a; device is ") + prop.name);
+        ctx->num_sms = prop.multiProcessorCount;
+        ctx->smem_optin = prop.sharedMemPerBlockOptin;
+        if (stream) {
+            ctx->stream = static_cast<cudaStream_t>(stream);
+        } else {
+            CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+            ctx->own_stream = true;
+        }
+    });
+    if (rc != EPC_OK) {
+        static thread_local std::string keep;
+        keep = ctx->last_error;
+        delete ctx;
+        return rc;
+    }
+    *out = ctx;
+    return EPC_OK;
+}
+
+void epc_context_destroy(epc_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto& b : ctx->bufs)
+        if (b.ptr) cudaFree(b.ptr);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    for (auto& pe : ctx->prof_pending) {
+        cudaEventDestroy(pe.start);
+        cudaEventDestroy(pe.stop);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int epc_set_stream(epc_context* ctx, void* stream) {
+    return guarded(ctx, [&] {
+        if (ctx->own_stream) {
+            CK(cudaStreamSynchronize(ctx->stream));
+            CK(cudaStreamDestroy(ctx->stream));
+            ctx->own_stream = false;
+        }
+        if (stream) ctx->stream = static_cast<cudaStream_t>(stream);
+        else {
+            CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+            ctx->own_stream = true;
+        }
+    });
+}
+
+const char* epc_last_error(const epc_context* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+int epc_set_mode(epc_context* ctx, int mode_bits) {
+    return guarded(ctx, [&] {
+        if ((mode_bits & EPC_MODE_BSTEP_TIMING) && !(ctx->mode & EPC_MODE_BSTEP_TIMING)) {
+            long long* t = slot_t<long long>(ctx, S_GN9, 16);
+            CK(cudaMemsetAsync(t, 0, 16 * sizeof(long long), ctx->stream));
+        }
+        ctx->mode = mode_bits;
+    });
+}
+
+int epc_bstep_timing(epc_context* ctx, long long* out10) {
+    return guarded(ctx, [&] {
+        long long* t = slot_t<long long>(ctx, S_GN9, 16);
+        d2h(ctx, out10, t, 10 * sizeof(long long));
+        sync(ctx);
+    });
+}
+
+int epc_profile_enable(epc_context* ctx, int on) {
+    if (!on && ctx->profiling) prof_drain(ctx);
+    ctx->profiling = on != 0;
+    return EPC_OK;
+}
+
+int epc_profile_read(epc_context* ctx, const char** names, double* total_ms, long* launches,
+                     int cap, int* count) {
+    prof_drain(ctx);
+    const int n = (int)ctx->prof_acc.size();
+    for (int i = 0; i < n && i < cap; ++i) {
+        names[i] = ctx->prof_acc[i].name;
+        total_ms[i] = ctx->prof_acc[i].ms;
+        launches[i] = ctx->prof_acc[i].n;
+    }
+    if (count) *count = n;
+    return EPC_OK;
+}
+
+void epc_profile_reset(epc_context* ctx) {
+    prof_drain(ctx);
+    ctx->prof_acc.clear();
+}
+
+long epc_launch_count(const epc_context* ctx) { return ctx->launches; }
+void epc_reset_launch_count(epc_context* ctx) { ctx->launches = 0; }
+
+int epc_admm_solve(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+                   const double* iminus, const double* b_in, const double* z_in,
+                   const double* u_in, double* b_out, double* z_out, double* u_out, double* rho,
+                   const epc_objective_params* p, const epc_admm_config* cfg, int level_tag,
+                   epc_admm_row* rows, int max_rows, epc_solve_status* status) {
+    return admm_solve_impl(ctx, g, 1, mem, iplus, iminus, b_in, z_in, u_in, b_out, z_out, u_out,
+                           rho, p, cfg, level_tag, rows, max_rows, status);
+}
+
+int epc_admm_solve_batch(epc_context* ctx, const epc_grid* g, int npairs, int mem,
+                         const double* iplus, const double* iminus, const double* b_in,
+                         const double* z_in, const double* u_in, double* b_out, double* z_out,
+                         double* u_out, double* rho, const epc_objective_params* p,
+                         const epc_admm_config* cfg, int level_tag, epc_admm_row* rows,
+                         int max_rows, epc_solve_status* status) {
+    if (npairs < 1) return EPC_ERR_INVALID_ARGUMENT;
+    return admm_solve_impl(ctx, g, npairs, mem, iplus, iminus, b_in, z_in, u_in, b_out, z_out,
+                           u_out, rho, p, cfg, level_tag, rows, max_rows, status);
+}
+
+int epc_b_update(epc_context* ctx, const epc_grid* gg, int mem, const double* iplus,
+                 const double* iminus, const double* b, const double* z, const double* u,
+                 double rho, const epc_objective_params* p, const epc_admm_config* cfg,
+                 double* b_out, epc_bupdate_stats* stats) {
+    return guarded(ctx, [&] {
+        const Geo g = make_geo(gg);
+        if (!(rho > 0.0)) fail(EPC_ERR_INVALID_ARGUMENT, "b_update: rho must be positive");
+        const size_t nc = g.ncell, nf = g.nface;
+        const double* ip = mem == EPC_MEM_DEVICE ? iplus : stage_in(ctx, S_IP, mem, iplus, nc);
+        const double* im = mem == EPC_MEM_DEVICE ? iminus : stage_in(ctx, S_IM, mem, iminus, nc);
+        double* bd = stage_in(ctx, S_B0, mem, b, nf);
+        double* zd = stage_in(ctx, S_Z0, mem, z, nf);
+        double* ud = stage_in(ctx, S_U0, mem, u, nf);
+        double* bo = slot_t<double>(ctx, S_B1, nf);
+        double* rd = slot_t<double>(ctx, S_PAIR, 4);
+        h2d(ctx, rd, &rho, sizeof(double));
+        BStepRun br = run_bstep(ctx, g, 1, ip, im, bd, zd, ud, bo, rd, nullptr, p->alpha, cfg);
+        double* sd = slot_t<double>(ctx, S_SCAL, 4);
+        long long* si = slot_t<long long>(ctx, S_TMP1, 6);
+        const long long total = g.ncol;
+        EPC_LAUNCH(ctx, "reduce_columns", k_reduce_columns, 1, 256, 0, br.col_i, br.col_i + total,
+                   br.col_i + 2 * total, br.col_i + 3 * total, br.col_d, br.col_d + total,
+                   br.col_d + 2 * total, g.ncol, nullptr, sd, si);
+        double hd[4];
+        long long hi[6];
+        d2h(ctx, hd, sd, sizeof hd);
+        d2h(ctx, hi, si, sizeof hi);
+        sync(ctx);
+        if (hi[0] >= 0) {
+            char m[256];
+            std::snprintf(m, sizeof m, "b_update: column %lld: %s", hi[0], qp_what((int)hi[1]));
+            fail(EPC_ERR_RUNTIME, m);
+        }
+        stage_out(ctx, mem, b_out, bo, nf);
+        sync(ctx);
+        if (stats) {
+            stats->sqp_iters = (long)hi[2];
+            stats->qp_iters = (long)hi[3];
+            stats->kkt_violation = hd[0];
+            stats->max_active = (int)hi[4];
+        }
+    });
+}
+
+int epc_dct_solve(epc_context* ctx, const epc_grid* gg, int mem, const double* rhs, double alpha,
+                  double rho, double* out) {
+    return guarded(ctx, [&] {
+        const Geo g = make_geo(gg);
+        if (!(alpha > 0.0)) fail(EPC_ERR_INVALID_ARGUMENT, "dct_coupled_solve: alpha must be > 0");
+        if (!(rho > 0.0)) fail(EPC_ERR_INVALID_ARGUMENT, "dct_coupled_solve: rho must be > 0");
+        const size_t nf = g.nface;
+        double* rd = stage_in(ctx, S_B0, mem, rhs, nf);
+        double* zo = slot_t<double>(ctx, S_Z1, nf);
+        const DctMats M = upload_dct(ctx, g);
+        double* rh = slot_t<double>(ctx, S_PAIR, 4);
+        h2d(ctx, rh, &rho, sizeof(double));
+        ZArgs za{};
+        za.b = rd;
+        za.u = rd;
+        za.z_new = zo;
+        za.rho = rh;
+        za.alpha = alpha;
+        za.rhs_is_raw = true;
+        run_zstep(ctx, g, 1, M, za);
+        stage_out(ctx, mem, out, zo, nf);
+        sync(ctx);
+    });
+}
+
+int epc_z_update(epc_context* ctx, const epc_grid* gg, int mem, const double* b, const double* u,
+                 double rho, double alpha, double* z_out) {
+    return guarded(ctx, [&] {
+        const Geo g = make_geo(gg);
+        if (!(alpha > 0.0)) fail(EPC_ERR_INVALID_ARGUMENT, "dct_coupled_solve: alpha must be > 0");
+        if (!(rho > 0.0)) fail(EPC_ERR_INVALID_ARGUMENT, "dct_coupled_solve: rho must be > 0");
+        const size_t nf = g.nface;
+        double* bd = stage_in(ctx, S_B0, mem, b, nf);
+        double* ud = stage_in(ctx, S_U0, mem, u, nf);
+        double* zo = slot_t<double>(ctx, S_Z1, nf);
+        const DctMats M = upload_dct(ctx, g);
+        double* rh = slot_t<double>(ctx, S_PAIR, 4);
+        h2d(ctx, rh, &rho, sizeof(double));
+        ZArgs za{};
+        za.b = bd;
+        za.u = ud;
+        za.z_new = zo;
+        za.rho = rh;
+        za.alpha = alpha;
+        run_zstep(ctx, g, 1, M, za);
+        stage_out(ctx, mem, z_out, zo, nf);
+        sync(ctx);
+    });
+}
+
+int epc_dual_update(epc_context* ctx, const epc_grid* gg, int mem, const double* b_new,
+                    const double* z_new, const double* z_old, const double* u_old, double rho,
+                    double eps_abs, double eps_rel, double* u_out, epc_dual_result* out) {
+    return guarded(ctx, [&] {
+        // The fused path computes this inside the z-step epilogue; this entry
+        // point evaluates the same element-wise update and sums standalone.
+        const Geo g = make_geo(gg);
+        const size_t nf = g.nface;
+        double* bd = stage_in(ctx, S_B0, mem, b_new, nf);
+        double* zn = stage_in(ctx, S_Z0, mem, z_new, nf);
+        double* zo = stage_in(ctx, S_Z1, mem, z_old, nf);
+        double* uo = stage_in(ctx, S_U0, mem, u_old, nf);
+        double* un = slot_t<double>(ctx, S_U1, nf);
+        const int nb = 128;
+        double* part = slot_t<double>(ctx, S_PART, (size_t)nb * 6);
+        EPC_LAUNCH(ctx, "dual_update", k_dual_standalone, nb, 256, 0, bd, zn, zo, uo, un, (long long)nf, part);
+        double* s = slot_t<double>(ctx, S_SCAL, 6);
+        EPC_LAUNCH(ctx, "reduce_dual", k_reduce_partials, 1, 256, 0, part, nb, 6, 6, s);
+        check_launch();
+        double hs[6];
+        d2h(ctx, hs, s, sizeof hs);
+        stage_out(ctx, mem, u_out, un, nf);
+        sync(ctx);
+        const double V = g.V;
+        const double sqrt_n = std::sqrt((double)g.nface);
+        if (out) {
+            out->primal_res = std::sqrt(hs[0]);
+            out->dual_res = rho * V * std::sqrt(hs[1]);
+            out->eps_pri = sqrt_n * eps_abs + eps_rel * std::max(std::sqrt(hs[2]), std::sqrt(hs[3]));
+            out->eps_dual = sqrt_n * eps_abs + eps_rel * rho * V * std::sqrt(hs[4]);
+        }
+    });
+}
+
+int epc_augmented_lagrangian(epc_context* ctx, const epc_grid* gg, int mem, const double* iplus,
+                             const double* iminus, const double* b, const double* z,
+                             const double* u, double rho, double alpha, double* out) {
+    return guarded(ctx, [&] {
+        const Geo g = make_geo(gg);
+        const size_t nc = g.ncell, nf = g.nface;
+        const double* ip = mem == EPC_MEM_DEVICE ? iplus : stage_in(ctx, S_IP, mem, iplus, nc);
+        const double* im = mem == EPC_MEM_DEVICE ? iminus : stage_in(ctx, S_IM, mem, iminus, nc);
+        double* bd = stage_in(ctx, S_B0, mem, b, nf);
+        double* zd = stage_in(ctx, S_Z0, mem, z, nf);
+        double* ud = stage_in(ctx, S_U0, mem, u, nf);
+        const int nb = 128;
+        double* part = slot_t<double>(ctx, S_PART, (size_t)nb * 4);
+        EPC_LAUNCH(ctx, "lagr_sums", k_lagr_sums, nb, 256, 0, ip, im, bd, zd, ud, g.m1, g.n1,
+                   g.ncell, g.nface, make_hdiv(g.h1), g.o1, part);
+        double* zp = slot_t<double>(ctx, S_PART2, (size_t)64 * 2);
+        EPC_LAUNCH(ctx, "zdiff_sums", k_zdiff_sums, dim3(64, 1), 256, 0, zd, g.nface, g.n1, g.m2,
+                   g.m3, 1.0 / g.h2, 1.0 / g.h3, zp);
+        double* s = slot_t<double>(ctx, S_SCAL, 6);
+        EPC_LAUNCH(ctx, "reduce_lagr", k_reduce_partials, 1, 256, 0, part, nb, 4, 4, s);
+        EPC_LAUNCH(ctx, "reduce_zdiff", k_reduce_partials, 1, 256, 0, zp, 64, 2, 2, s + 4);
+        check_launch();
+        double hs[6];
+        d2h(ctx, hs, s, sizeof hs);
+        sync(ctx);
+        const double V = g.V;
+        const double fval = 0.5 * V * hs[0] + 0.5 * alpha * V * hs[1];
+        double gs = hs[4];
+        if (g.dim == 3) gs += hs[5];
+        const double gval = 0.5 * alpha * V * gs;
+        *out = fval + gval + rho * V * hs[2] + 0.5 * rho * V * hs[3];
+    });
+}
+
+double epc_rho_schedule(int schedule, double rho, double rho_min, double primal_res,
+                        double dual_res, double tau_incr, double tau_decr, double mu) {
+    return rho_schedule(schedule, rho, rho_min, primal_res, dual_res, tau_incr, tau_decr, mu);
+}
+
+int epc_qp_active_set_batch(epc_context* ctx, int nqp, int n, double h, const double* gd,
+                            const double* go, const double* c, const double* x0, int max_iter,
+                            double* x, double* lambda, int* active_sign, int* iters, double* kkt,
+                            int* status) {
+    return guarded(ctx, [&] {
+        if (nqp < 1 || n < 2) fail(EPC_ERR_INVALID_ARGUMENT, "qp batch: need nqp >= 1, n >= 2");
+        const size_t nv = (size_t)nqp * n, nl = (size_t)nqp * (n - 1);
+        double* dgd = stage_in(ctx, S_TMP0, EPC_MEM_HOST, gd, nv);
+        double* dgo = stage_in(ctx, S_H1, EPC_MEM_HOST, go, nv);
+        double* dc = stage_in(ctx, S_H2, EPC_MEM_HOST, c, nv);
+        double* dx0 = stage_in(ctx, S_B0, EPC_MEM_HOST, x0, nv);
+        double* dx = slot_t<double>(ctx, S_B1, nv);
+        double* dl = slot_t<double>(ctx, S_Z0, nl);
+        int* ds = slot_t<int>(ctx, S_COLI, nl + 3 * (size_t)nqp);
+        double* dk = slot_t<double>(ctx, S_Z1, nqp);
+        const size_t smem = bstep_smem_bytes(n);
+        if (smem > ctx->smem_optin) fail(EPC_ERR_UNSUPPORTED, "QP too long for shared memory");
+        CK(cudaFuncSetAttribute(k_qp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_optin));
+        const int blocks = std::min(nqp, ctx->num_sms * 8);
+        const int qcap = n - 1;
+        QpBatchParams P{};
+        P.nqp = nqp;
+        P.n = n;
+        P.dh = make_hdiv(h);
+        P.gd = dgd;
+        P.go = dgo;
+        P.c = dc;
+        P.x0 = dx0;
+        P.max_iter = max_iter;
+        P.x = dx;
+        P.lambda = dl;
+        P.sign = ds;
+        P.iters = ds + nl;
+        P.status = ds + nl + nqp;
+        P.kkt = dk;
+        P.qbuf = slot_t<double>(ctx, S_QBUF, (size_t)blocks * qcap * n);
+        P.sbuf = slot_t<double>(ctx, S_SBUF, (size_t)blocks * qcap * qcap);
+        P.qcap = qcap;
+        EPC_LAUNCH(ctx, "qp_batch", k_qp_batch, blocks, 32, smem, P);
+        check_launch();
+        std::vector<int> st(nqp);
+        d2h(ctx, x, dx, nv * sizeof(double));
+        d2h(ctx, lambda, dl, nl * sizeof(double));
+        d2h(ctx, active_sign, ds, nl * sizeof(int));
+        d2h(ctx, iters, ds + nl, (size_t)nqp * sizeof(int));
+        d2h(ctx, st.data(), ds + nl + nqp, (size_t)nqp * sizeof(int));
+        if (kkt) d2h(ctx, kkt, dk, (size_t)nqp * sizeof(double));
+        sync(ctx);
+        int first = -1;
+        for (int q = 0; q < nqp; ++q) {
+            // std::invalid_argument for an infeasible start, runtime_error otherwise
+            status[q] = st[q] == 0 ? EPC_OK : (st[q] == 2 ? EPC_ERR_INVALID_ARGUMENT : EPC_ERR_RUNTIME);
+            if (st[q] != 0 && first < 0) first = q;
+        }
+        if (first >= 0) ctx->last_error = qp_what(st[first]);
+    });
+}
+
+int epc_residual(epc_context* ctx, const epc_grid* gg, int mem, const double* iplus,
+                 const double* iminus, const double* b, double* r) {
+    return guarded(ctx, [&] {
+        const Geo g = make_geo(gg);
+        const size_t nc = g.ncell, nf = g.nface;
+        const double* ip = mem == EPC_MEM_DEVICE ? iplus : stage_in(ctx, S_IP, mem, iplus, nc);
+        const double* im = mem == EPC_MEM_DEVICE ? iminus : stage_in(ctx, S_IM, mem, iminus, nc);
+        double* bd = stage_in(ctx, S_B0, mem, b, nf);
+        double* rd = slot_t<double>(ctx, S_TMP0, nc);
+        EPC_LAUNCH(ctx, "residual", k_residual, grid1d(ctx, (long long)nc), 256, 0, ip, im, bd,
+                   g.m1, g.n1, g.ncell, make_hdiv(g.h1), g.o1, rd);
+        check_launch();
+        stage_out(ctx, mem, r, rd, nc);
+        sync(ctx);
+    });
+}
+
+const char* epc_build_info(void) {
+    return "libepicorr_b200 sm_100a fp64 exact (-fmad=false, IEEE div/sqrt)";
+}
+
+}  // extern "C"
+

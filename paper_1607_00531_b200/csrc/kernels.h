@@ -1,0 +1,113 @@
+// kernels.h — kernel parameter blocks and launch helpers shared by api.cu.
+#pragma once
+
+#include "common.cuh"
+#include "model.cuh"
+
+// ---- ADMM b-step (bstep.cu) ---------------------------------------------
+struct BStepParams {
+    int m1, n1;
+    long long ncol;  // columns per pair
+    long long ncell, nface;
+    HDiv dh;         // spacing h1 and its exact-division mode
+    double o1, V, alpha;
+    const double *ip, *im, *b, *z, *u;
+    double* b_out;
+    const double* rho;  // [npairs]
+    const int* active;  // [npairs] or nullptr
+    int sqp_max_iter;
+    double sqp_tol_rel;
+    int check_kkt, qp_cap;
+    int *col_err, *col_sqp, *col_qp, *col_maxact;
+    double *col_kkt, *col_fr, *col_fd;
+    double *qbuf, *sbuf;
+    int qcap;
+    unsigned long long* counter;
+    long long total_cols;
+    long long* timing;  // optional [10] phase cycle totals (lane 0), nullptr = off
+};
+__global__ void k_admm_bstep(BStepParams P);
+
+struct QpBatchParams {
+    int nqp, n;
+    HDiv dh;
+    const double *gd, *go, *c, *x0;
+    int max_iter;
+    double *x, *lambda;
+    int *sign, *iters;
+    double* kkt;
+    int* status;
+    double *qbuf, *sbuf;
+    int qcap;
+};
+__global__ void k_qp_batch(QpBatchParams P);
+size_t bstep_smem_bytes(int n1);
+
+// ---- dense DCT z-step (zstep.cu) ------------------------------------------
+// Out[row][col] = sum_k A[row][k] * In[k][col], k ascending, unfused mul/add.
+// Element (k, col) of an operand lives at k*kstride + (col/cdiv)*cstride + col%cdiv
+// (+ blockIdx.z * zstride for a batch of independent volumes).
+struct GemmParams {
+    const double* A;  // M x K row-major
+    int M, K;
+    long long N;
+    const double *in0, *in1;  // in1 only for the rhs prologue
+    long long kstride, cdiv, cstride, zstride;
+    double* out;
+    // prologue: B = rho[pair] * V * (in0 + in1)
+    const double* rho;
+    double V;
+    long long nface;  // for pair = face / nface
+    // divide epilogue
+    const double* lam23;
+    double alpha;
+    int m2, n1, m3;
+    int div_axis;  // 3: row = q3, j = col / n1; 2: row = q2, k = col / n1
+    // dual epilogue
+    const double *bvec, *u_old, *z_old;
+    double* u_new;
+    double* partials;  // per CTA: 6 sums
+    const int* active;
+};
+enum { PRO_PLAIN = 0, PRO_RHS = 1 };
+enum { EPI_STORE = 0, EPI_DIVIDE = 1, EPI_DUAL = 2 };
+void launch_dct_gemm(epc_context* ctx, const char* name, const GemmParams& p, int pro, int epi,
+                     int nz, int* nblocks_out);
+
+// Sum of squared D2 / D3 differences of z (g_value, admm.cpp:275-285): per CTA
+// partials [2] over faces of all pairs.
+__global__ void k_zdiff_sums(const double* z, long long nface_total, int n1, int m2, int m3,
+                             double ih2, double ih3, double* partials);
+
+// Fixed-order reduction of per-block partials: out[s] = sum_b in[b*stride + s]
+// for s < nsum, segment per pair (pairs x nblk_per_pair blocks).
+__global__ void k_reduce_partials(const double* in, int nblk, int stride, int nsum,
+                                  double* out);
+
+// ---- per-column b-step statistics -> per pair scalars ---------------------
+__global__ void k_reduce_columns(const int* col_err, const int* col_sqp, const int* col_qp,
+                                 const int* col_maxact, const double* col_kkt,
+                                 const double* col_fr, const double* col_fd, long long ncol,
+                                 const int* active, double* out_d, long long* out_i);
+
+// ---- element-wise helpers ---------------------------------------------------
+__global__ void k_scale_pairs(double* u, long long nface, int npairs, const double* factor);
+__global__ void k_copy_masked(const double* src, double* dst, long long nface, int npairs,
+                              const int* mask);
+
+// aux_kernels.cu
+__global__ void k_residual(const double* ip, const double* im, const double* b, int m1, int n1,
+                           long long ncell, HDiv dh, double o1, double* r);
+__global__ void k_lagr_sums(const double* ip, const double* im, const double* b, const double* z,
+                            const double* u, int m1, int n1, long long ncell, long long nface,
+                            HDiv dh, double o1, double* partials);
+
+__global__ void k_dual_standalone(const double* b, const double* zn, const double* zo,
+                                  const double* uo, double* un, long long n, double* partials);
+
+// ---- GN (gn.cu) -------------------------------------------------------------
+struct GnGeom {
+    int m1, n1, m2, m3, dim;
+    long long ncol, ncell, nface;
+    double h1, h2, h3, o1, V;
+};

@@ -1,0 +1,325 @@
+// zstep.cu — ADMM z-step and dual update on sm_100a.
+//
+// The reference z-step (z_update, proj/src/admm.cpp:445-451, through
+// DctCoupledSolver::solve, proj/src/operators.cpp:388-418) applies dense
+// orthonormal DCT-II matrices along axes 2 and 3 (transform_axis2/3,
+// operators.cpp:347-386): out[q][.] = sum_j C[q][j] in[j][.], j ascending,
+// starting from 0. Each transform is therefore a small-M GEMM whose
+// K-loop order we keep: every output accumulates k = 0..K-1 in order with
+// separate multiply and add (-fmad=false), so z is bitwise the reference's.
+// rhs formation (rho*V*(b+u)) is fused into the first GEMM's operand load,
+// the spectral divide into the axis-3 forward GEMM's epilogue and the dual
+// update (dual_update_and_residuals, admm.cpp:453-476) plus the residual /
+// Lagrangian partial sums into the last GEMM's epilogue.
+//
+// Tiling: 64x64 output tile per 256-thread CTA, 16-deep K slabs staged in
+// shared memory with register prefetch of the next slab; each thread owns a
+// 4x4 strided sub-tile (conflict-free/broadcast shared loads). fp64 has no
+// tensor-core path on this part that preserves the reference's rounding, so
+// this is an FP64-pipe kernel by design.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
+}
+
+template <int PRO, int EPI>
+__global__ void __launch_bounds__(NT) k_dct_gemm(GemmParams p) {
+    __shared__ double As[BK][BM];
+    __shared__ double Bs[BK][BN];
+    __shared__ double red[(NT / 32) * 6];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int row0 = blockIdx.y * BM;
+    const long long col0 = (long long)blockIdx.x * BN;
+    const int pair = blockIdx.z;
+    const long long zoff = (long long)pair * p.zstride;
+
+    // this thread's B-load column (fixed across the K loop)
+    const int ln = tid & 63, lk = tid >> 6;  // 4 rows lk, lk+4, lk+8, lk+12
+    const long long lcol = col0 + ln;
+    const bool lcol_ok = lcol < p.N;
+    const long long lmap = lcol_ok ? (lcol / p.cdiv) * p.cstride + (lcol % p.cdiv) : 0;
+    double wrhs = 0.0;
+    if (PRO == PRO_RHS) wrhs = p.rho[pair] * p.V;
+    // this thread's A-load element
+    const int am = tid >> 4 /*0..15*/, ak = tid & 15;
+
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+
+    double ra[4], rb[4];
+    auto load_tile = [&](int k0) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int m = am + 16 * t, k = k0 + ak;
+            ra[t] = (row0 + m < p.M && k < p.K) ? __ldg(p.A + (size_t)(row0 + m) * p.K + k) : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int k = k0 + lk + 4 * t;
+            double v = 0.0;
+            if (lcol_ok && k < p.K) {
+                const long long a = zoff + (long long)k * p.kstride + lmap;
+                if (PRO == PRO_RHS) v = wrhs * (__ldg(p.in0 + a) + __ldg(p.in1 + a));
+                else v = __ldg(p.in0 + a);
+            }
+            rb[t] = v;
+        }
+    };
+
+    load_tile(0);
+    for (int k0 = 0; k0 < p.K; k0 += BK) {
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 4; ++t) As[ak][am + 16 * t] = ra[t];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) Bs[lk + 4 * t][ln] = rb[t];
+        __syncthreads();
+        if (k0 + BK < p.K) load_tile(k0 + BK);
+        const int kend = min(BK, p.K - k0);
+        if (kend == BK) {
+#pragma unroll
+            for (int kk = 0; kk < BK; ++kk) {
+                double a[4], b[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[r][c] = acc[r][c] + a[r] * b[c];
+            }
+        } else {
+            for (int kk = 0; kk < kend; ++kk) {
+                double a[4], b[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[r][c] = acc[r][c] + a[r] * b[c];
+            }
+        }
+    }
+
+    double ps[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    const bool act = (EPI == EPI_DUAL) ? (p.active == nullptr || p.active[pair] != 0) : true;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const long long col = col0 + tx + 16 * c;
+        if (col >= p.N) continue;
+        const long long cmap = (col / p.cdiv) * p.cstride + (col % p.cdiv);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int row = row0 + ty + 16 * r;
+            if (row >= p.M) continue;
+            const long long f = zoff + (long long)row * p.kstride + cmap;
+            double v = acc[r][c];
+            if (EPI == EPI_DIVIDE) {
+                int cidx;
+                if (p.div_axis == 3) cidx = (int)(col / p.n1) + p.m2 * row;
+                else cidx = row + p.m2 * (int)((col / p.n1) % p.m3);
+                const double denom = p.alpha * p.V * p.lam23[cidx] + p.rho[pair] * p.V;
+                p.out[f] = v / denom;
+            } else if (EPI == EPI_DUAL) {
+                if (act) {
+                    p.out[f] = v;
+                    const double bb = p.bvec[f];
+                    const double diff = bb - v;
+                    const double un = p.u_old[f] + diff;
+                    p.u_new[f] = un;
+                    const double dz = p.z_old[f] - v;
+                    ps[0] += diff * diff;
+                    ps[1] += dz * dz;
+                    ps[2] += bb * bb;
+                    ps[3] += v * v;
+                    ps[4] += un * un;
+                    ps[5] += un * diff;
+                } else {
+                    p.out[f] = p.z_old[f];
+                    p.u_new[f] = p.u_old[f];
+                }
+            } else {
+                p.out[f] = v;
+            }
+        }
+    }
+    if (EPI == EPI_DUAL) {
+        const int w = tid >> 5, l = tid & 31;
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+            const double v = warp_sum(ps[s]);
+            if (l == 0) red[w * 6 + s] = v;
+        }
+        __syncthreads();
+        if (tid < 6) {
+            double t = 0.0;
+            for (int i = 0; i < NT / 32; ++i) t += red[i * 6 + tid];
+            const long long blk = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+            const long long nblk = (long long)gridDim.x * gridDim.y;
+            p.partials[((long long)pair * nblk + blk) * 6 + tid] = t;
+        }
+    }
+}
+
+void launch_dct_gemm(epc_context* ctx, const char* name, const GemmParams& p, int pro, int epi,
+                     int nz, int* nblocks_out) {
+    dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + BM - 1) / BM), (unsigned)nz);
+    if (nblocks_out) *nblocks_out = (int)(grid.x * grid.y);
+    if (pro == PRO_RHS && epi == EPI_STORE)
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_STORE>), grid, NT, 0, p);
+    else if (pro == PRO_RHS && epi == EPI_DIVIDE)
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_DIVIDE>), grid, NT, 0, p);
+    else if (pro == PRO_PLAIN && epi == EPI_DIVIDE)
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DIVIDE>), grid, NT, 0, p);
+    else if (pro == PRO_PLAIN && epi == EPI_DUAL)
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DUAL>), grid, NT, 0, p);
+    else
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_STORE>), grid, NT, 0, p);
+}
+
+// g_value parts (admm.cpp:275-285): sum over faces of (D2 z)^2 and (D3 z)^2,
+// differences scaled by 1/h exactly as diff_perp (operators.cpp:70-100).
+// grid: (blocks, npairs); partials[(pair*gridDim.x + blk)*2 + {0,1}].
+__global__ void __launch_bounds__(256) k_zdiff_sums(const double* z, long long nface, int n1,
+                                                   int m2, int m3, double ih2, double ih3,
+                                                   double* partials) {
+    __shared__ double sh[16];
+    const int pair = blockIdx.y;
+    const double* zp = z + (long long)pair * nface;
+    const long long layer = (long long)n1 * m2;
+    double s2 = 0.0, s3 = 0.0;
+    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < nface;
+         f += (long long)gridDim.x * blockDim.x) {
+        const long long c = f / n1;
+        const int j = (int)(c % m2), k = (int)(c / m2);
+        const double zf = zp[f];
+        if (j + 1 < m2) {
+            const double o = (zp[f + n1] - zf) * ih2;
+            s2 += o * o;
+        }
+        if (m3 > 1 && k + 1 < m3) {
+            const double o = (zp[f + layer] - zf) * ih3;
+            s3 += o * o;
+        }
+    }
+    const double t2 = block_sum(s2, sh);
+    const double t3 = block_sum(s3, sh + 8);
+    if (threadIdx.x == 0) {
+        partials[((long long)pair * gridDim.x + blockIdx.x) * 2 + 0] = t2;
+        partials[((long long)pair * gridDim.x + blockIdx.x) * 2 + 1] = t3;
+    }
+}
+
+// out[pair*nsum + s] = sum over blk of in[(pair*nblk + blk)*stride + s]; one
+// CTA per pair, fixed order (strided per-thread scan + fixed tree).
+__global__ void __launch_bounds__(256) k_reduce_partials(const double* in, int nblk, int stride,
+                                                        int nsum, double* out) {
+    __shared__ double sh[8];
+    const int pair = blockIdx.x;
+    for (int s = 0; s < nsum; ++s) {
+        double v = 0.0;
+        for (int b = threadIdx.x; b < nblk; b += blockDim.x)
+            v += in[((long long)pair * nblk + b) * stride + s];
+        const double t = block_sum(v, sh);
+        if (threadIdx.x == 0) out[pair * nsum + s] = t;
+        __syncthreads();
+    }
+}
+
+// Per-pair reduction of the b-step's per-column outputs. out_d[pair*4]:
+// {kkt max, sum r^2, sum (D1 b)^2, 0}; out_i[pair*6]: {first failing column or
+// -1, its error code, sqp total, qp total, max active, 0}.
+__global__ void __launch_bounds__(256) k_reduce_columns(const int* col_err, const int* col_sqp,
+                                                       const int* col_qp, const int* col_maxact,
+                                                       const double* col_kkt, const double* col_fr,
+                                                       const double* col_fd, long long ncol,
+                                                       const int* active, double* out_d,
+                                                       long long* out_i) {
+    __shared__ double sh[8];
+    __shared__ long long shi[8][4];
+    const int pair = blockIdx.x;
+    if (active && !active[pair]) return;
+    const long long base = (long long)pair * ncol;
+    double kk = 0.0, fr = 0.0, fd = 0.0;
+    long long first = 0x7fffffffffffffffLL, sqp = 0, qp = 0, mact = 0;
+    for (long long c = threadIdx.x; c < ncol; c += blockDim.x) {
+        const long long g = base + c;
+        if (col_err[g] != 0 && c < first) first = c;
+        sqp += col_sqp[g];
+        qp += col_qp[g];
+        mact = max(mact, (long long)col_maxact[g]);
+        kk = dmax_ref(kk, col_kkt[g]);
+        fr += col_fr[g];
+        fd += col_fd[g];
+    }
+    const double tfr = block_sum(fr, sh);
+    __syncthreads();
+    const double tfd = block_sum(fd, sh);
+    __syncthreads();
+    // max / min / integer sums (exact in any order)
+    double km = warp_max(kk);
+    for (int o = 16; o > 0; o >>= 1) {
+        first = min(first, __shfl_xor_sync(FULL_MASK, first, o));
+        sqp += __shfl_xor_sync(FULL_MASK, sqp, o);
+        qp += __shfl_xor_sync(FULL_MASK, qp, o);
+        mact = max(mact, __shfl_xor_sync(FULL_MASK, mact, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sh[w] = km;
+        shi[w][0] = first;
+        shi[w][1] = sqp;
+        shi[w][2] = qp;
+        shi[w][3] = mact;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int nw = blockDim.x >> 5;
+        double K = 0.0;
+        long long F = 0x7fffffffffffffffLL, S = 0, Q = 0, M = 0;
+        for (int i = 0; i < nw; ++i) {
+            K = dmax_ref(K, sh[i]);
+            F = min(F, shi[i][0]);
+            S += shi[i][1];
+            Q += shi[i][2];
+            M = max(M, shi[i][3]);
+        }
+        out_d[pair * 4 + 0] = K;
+        out_d[pair * 4 + 1] = tfr;
+        out_d[pair * 4 + 2] = tfd;
+        out_d[pair * 4 + 3] = 0.0;
+        const bool bad = F != 0x7fffffffffffffffLL;
+        out_i[pair * 6 + 0] = bad ? F : -1;
+        out_i[pair * 6 + 1] = bad ? col_err[base + F] : 0;
+        out_i[pair * 6 + 2] = S;
+        out_i[pair * 6 + 3] = Q;
+        out_i[pair * 6 + 4] = M;
+        out_i[pair * 6 + 5] = 0;
+    }
+}
+
+// u *= factor[pair] (scale(st.u.v, rho/next), admm.cpp:549-552)
+__global__ void k_scale_pairs(double* u, long long nface, int npairs, const double* factor) {
+    const long long n = nface * npairs;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double a = factor[i / nface];
+        if (a != 1.0) u[i] *= a;
+    }
+}
+
+__global__ void k_copy_masked(const double* src, double* dst, long long nface, int npairs,
+                              const int* mask) {
+    const long long n = nface * npairs;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        if (mask[i / nface]) dst[i] = src[i];
+}

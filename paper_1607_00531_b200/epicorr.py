@@ -1,0 +1,332 @@
+"""Host mirror of the reference epicorr solver API over libepicorr_b200.so.
+
+Names, argument meaning and error behaviour follow the reference's C++ entry
+points (proj/include/epicorr/admm.hpp, gn_pcg.hpp, objective.hpp,
+operators.hpp): `admm_solve`, `b_update`, `z_update`, `dual_update_and_
+residuals`, `augmented_lagrangian`, `rho_schedule`, `qp_active_set`,
+`gauss_newton_solve`, `objective_gn`, `GnHessian` parts, `pcg`. Errors the
+reference throws are raised as the matching Python exception
+(ValueError <- std::invalid_argument, RuntimeError <- std::runtime_error,
+ArithmeticError <- std::domain_error) with the reference's message text.
+
+Arrays: numpy float64 (host; copied through the call) or torch CUDA float64
+tensors (device; used in place, EPC_MEM_DEVICE). There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import abi
+from ._lib import load
+from .abi import (AdmmConfig, AdmmRow, BUpdateStats, DualResult, GnConfig, GnRow, Grid,
+                  ObjectiveEval, ObjectiveParams, PcgResult, SolveStatus)
+
+_EXC = {abi.EPC_ERR_INVALID_ARGUMENT: ValueError, abi.EPC_ERR_RUNTIME: RuntimeError,
+        abi.EPC_ERR_DOMAIN: ArithmeticError, abi.EPC_ERR_CUDA: OSError,
+        abi.EPC_ERR_UNSUPPORTED: NotImplementedError}
+
+
+class EpcError(Exception):
+    pass
+
+
+def _raise(code, msg):
+    raise _EXC.get(code, EpcError)(msg)
+
+
+def _is_dev(a):
+    return a is not None and hasattr(a, "is_cuda") and a.is_cuda
+
+
+class Context:
+    """One device context (epc_context). `stream`: a torch.cuda.Stream, a raw
+    cudaStream_t int, or None for a library-owned stream."""
+
+    def __init__(self, device=0, stream=None):
+        self.lib = load()
+        h = C.c_void_p()
+        raw = getattr(stream, "cuda_stream", stream)
+        rc = self.lib.epc_context_create(device, C.c_void_p(raw) if raw else None, C.byref(h))
+        if rc != 0:
+            _raise(rc, f"epc_context_create failed (status {rc})")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.epc_context_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- plumbing ---------------------------------------------------------
+    def _err(self):
+        return self.lib.epc_last_error(self.h).decode()
+
+    def _check(self, rc):
+        if rc != 0:
+            _raise(rc, self._err())
+
+    def _mem(self, *arrays):
+        dev = [_is_dev(a) for a in arrays if a is not None]
+        if any(dev) and not all(dev):
+            raise ValueError("mix of host and device arrays")
+        return abi.EPC_MEM_DEVICE if dev and dev[0] else abi.EPC_MEM_HOST
+
+    @staticmethod
+    def _ptr(a):
+        if a is None:
+            return None
+        if _is_dev(a):
+            assert a.dtype.__str__() == "torch.float64" and a.is_contiguous()
+            return C.c_void_p(a.data_ptr())
+        assert isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+        return C.c_void_p(a.ctypes.data)
+
+    def _like(self, ref, n):
+        if _is_dev(ref):
+            import torch
+            return torch.empty(n, dtype=torch.float64, device=ref.device)
+        return np.zeros(n)
+
+    def set_stream(self, stream):
+        raw = getattr(stream, "cuda_stream", stream)
+        self._check(self.lib.epc_set_stream(self.h, C.c_void_p(raw) if raw else None))
+
+    def launch_count(self):
+        return self.lib.epc_launch_count(self.h)
+
+    def reset_launch_count(self):
+        self.lib.epc_reset_launch_count(self.h)
+
+    def profile(self, on=True):
+        self.lib.epc_profile_enable(self.h, int(on))
+
+    def profile_reset(self):
+        self.lib.epc_profile_reset(self.h)
+
+    def set_mode(self, bits):
+        self._check(self.lib.epc_set_mode(self.h, int(bits)))
+
+    BSTEP_PHASES = ["model", "fval_sums", "factor", "solves", "qp_rest", "kkt", "step_sums",
+                    "line_search", "clamp_store", "fetch"]
+
+    def bstep_timing(self):
+        out = (C.c_longlong * 10)()
+        self._check(self.lib.epc_bstep_timing(self.h, out))
+        return dict(zip(self.BSTEP_PHASES, list(out)))
+
+    def profile_read(self):
+        cap = 64
+        names = (C.c_char_p * cap)()
+        ms = (C.c_double * cap)()
+        n = (C.c_long * cap)()
+        cnt = C.c_int(0)
+        self.lib.epc_profile_read(self.h, names, ms, n, cap, C.byref(cnt))
+        return {names[i].decode(): (ms[i], n[i]) for i in range(min(cnt.value, cap))}
+
+    # ---- ADMM -------------------------------------------------------------
+    def admm_solve(self, g: Grid, ip, im, b=None, z=None, u=None, rho=0.0, params=None, cfg=None,
+                   level_tag=0):
+        """admm_solve (admm.hpp:127-129). Returns dict(b, z, u, rho, stop, message, rows)."""
+        params = params or ObjectiveParams()
+        cfg = cfg or AdmmConfig()
+        mem = self._mem(ip, im, b, z, u)
+        nf = g.faces
+        bo, zo, uo = self._like(ip, nf), self._like(ip, nf), self._like(ip, nf)
+        rows = (AdmmRow * max(cfg.max_iter, 1))()
+        st = SolveStatus()
+        r = C.c_double(rho)
+        rc = self.lib.epc_admm_solve(self.h, C.byref(g), mem, self._ptr(ip), self._ptr(im),
+                                     self._ptr(b), self._ptr(z), self._ptr(u), self._ptr(bo),
+                                     self._ptr(zo), self._ptr(uo), C.byref(r), C.byref(params),
+                                     C.byref(cfg), level_tag, rows, cfg.max_iter, C.byref(st))
+        if rc != 0:
+            _raise(rc, self._err() or st.message.decode())
+        return dict(b=bo, z=zo, u=uo, rho=r.value, stop=st.stop, message=st.message.decode(),
+                    rows=abi.rows_to_dicts(rows, min(st.nrows, cfg.max_iter)))
+
+    def admm_solve_batch(self, g: Grid, npairs, ip, im, rho=None, params=None, cfg=None,
+                         level_tag=0):
+        params = params or ObjectiveParams()
+        cfg = cfg or AdmmConfig()
+        mem = self._mem(ip, im)
+        nf = g.faces * npairs
+        bo, zo, uo = self._like(ip, nf), self._like(ip, nf), self._like(ip, nf)
+        rows = (AdmmRow * (max(cfg.max_iter, 1) * npairs))()
+        st = (SolveStatus * npairs)()
+        rh = (C.c_double * npairs)(*([0.0] * npairs if rho is None else rho))
+        rc = self.lib.epc_admm_solve_batch(self.h, C.byref(g), npairs, mem, self._ptr(ip),
+                                           self._ptr(im), None, None, None, self._ptr(bo),
+                                           self._ptr(zo), self._ptr(uo), rh, C.byref(params),
+                                           C.byref(cfg), level_tag, rows, cfg.max_iter, st)
+        if rc != 0:
+            _raise(rc, self._err())
+        out = []
+        for q in range(npairs):
+            rr = [rows[q * cfg.max_iter + i] for i in range(min(st[q].nrows, cfg.max_iter))]
+            out.append(dict(stop=st[q].stop, message=st[q].message.decode(), rho=rh[q],
+                            rows=[{k: getattr(x, k) for k, _ in x._fields_} for x in rr]))
+        return dict(b=bo, z=zo, u=uo, pairs=out)
+
+    def b_update(self, g, ip, im, b, z, u, rho, params=None, cfg=None):
+        params = params or ObjectiveParams()
+        cfg = cfg or AdmmConfig()
+        mem = self._mem(ip, im, b, z, u)
+        out = self._like(b, g.faces)
+        st = BUpdateStats()
+        self._check(self.lib.epc_b_update(self.h, C.byref(g), mem, self._ptr(ip), self._ptr(im),
+                                          self._ptr(b), self._ptr(z), self._ptr(u), rho,
+                                          C.byref(params), C.byref(cfg), self._ptr(out),
+                                          C.byref(st)))
+        return dict(b=out, sqp_iters=st.sqp_iters, qp_iters=st.qp_iters,
+                    kkt_violation=st.kkt_violation, max_active=st.max_active)
+
+    def z_update(self, g, b, u, rho, alpha):
+        mem = self._mem(b, u)
+        out = self._like(b, g.faces)
+        self._check(self.lib.epc_z_update(self.h, C.byref(g), mem, self._ptr(b), self._ptr(u), rho,
+                                          alpha, self._ptr(out)))
+        return out
+
+    def dct_solve(self, g, rhs, alpha, rho):
+        mem = self._mem(rhs)
+        out = self._like(rhs, g.faces)
+        self._check(self.lib.epc_dct_solve(self.h, C.byref(g), mem, self._ptr(rhs), alpha, rho,
+                                           self._ptr(out)))
+        return out
+
+    def dual_update(self, g, b_new, z_new, z_old, u_old, rho, eps_abs, eps_rel):
+        mem = self._mem(b_new, z_new, z_old, u_old)
+        u = self._like(b_new, g.faces)
+        r = DualResult()
+        self._check(self.lib.epc_dual_update(self.h, C.byref(g), mem, self._ptr(b_new),
+                                             self._ptr(z_new), self._ptr(z_old), self._ptr(u_old),
+                                             rho, eps_abs, eps_rel, self._ptr(u), C.byref(r)))
+        return u, dict(primal_res=r.primal_res, dual_res=r.dual_res, eps_pri=r.eps_pri,
+                       eps_dual=r.eps_dual)
+
+    def augmented_lagrangian(self, g, ip, im, b, z, u, rho, alpha):
+        mem = self._mem(ip, im, b, z, u)
+        out = C.c_double()
+        self._check(self.lib.epc_augmented_lagrangian(self.h, C.byref(g), mem, self._ptr(ip),
+                                                      self._ptr(im), self._ptr(b), self._ptr(z),
+                                                      self._ptr(u), rho, alpha, C.byref(out)))
+        return out.value
+
+    def rho_schedule(self, *args):
+        return self.lib.epc_rho_schedule(*args)
+
+    def qp_active_set_batch(self, n, h, gd, go, c, x0, max_iter):
+        """Many independent column QPs (qp_active_set + verify_qp_kkt)."""
+        gd, go, c, x0 = (np.ascontiguousarray(a, dtype=np.float64) for a in (gd, go, c, x0))
+        nqp = gd.size // n
+        x = np.zeros(nqp * n)
+        lam = np.zeros(nqp * (n - 1))
+        sign = np.zeros(nqp * (n - 1), dtype=np.int32)
+        iters = np.zeros(nqp, dtype=np.int32)
+        kkt = np.zeros(nqp)
+        status = np.zeros(nqp, dtype=np.int32)
+        P = lambda a: C.c_void_p(a.ctypes.data)
+        self._check(self.lib.epc_qp_active_set_batch(self.h, nqp, n, h, P(gd), P(go), P(c), P(x0),
+                                                     max_iter, P(x), P(lam), P(sign), P(iters),
+                                                     P(kkt), P(status)))
+        return dict(x=x.reshape(nqp, n), lam=lam.reshape(nqp, n - 1),
+                    sign=sign.reshape(nqp, n - 1), iters=iters, kkt=kkt, status=status,
+                    message=self._err())
+
+    def residual(self, g, ip, im, b):
+        mem = self._mem(ip, im, b)
+        r = self._like(ip, g.cells)
+        self._check(self.lib.epc_residual(self.h, C.byref(g), mem, self._ptr(ip), self._ptr(im),
+                                          self._ptr(b), self._ptr(r)))
+        return r
+
+    # ---- GN-PCG -----------------------------------------------------------
+    def gn_solve(self, g, ip, im, b0=None, params=None, cfg=None, level_tag=0):
+        """gauss_newton_solve (gn_pcg.hpp:81-83)."""
+        params = params or ObjectiveParams()
+        cfg = cfg or GnConfig()
+        mem = self._mem(ip, im, b0)
+        if b0 is None:
+            b0 = self._like(ip, g.faces)
+            if not _is_dev(b0):
+                b0[:] = 0.0
+            else:
+                b0.zero_()
+        bo = self._like(ip, g.faces)
+        rows = (GnRow * (cfg.max_outer + 1))()
+        st = SolveStatus()
+        rc = self.lib.epc_gn_solve(self.h, C.byref(g), mem, self._ptr(ip), self._ptr(im),
+                                   self._ptr(b0), self._ptr(bo), C.byref(params), C.byref(cfg),
+                                   level_tag, rows, cfg.max_outer + 1, C.byref(st))
+        if rc != 0:
+            _raise(rc, self._err())
+        return dict(b=bo, stop=st.stop, message=st.message.decode(),
+                    rows=abi.rows_to_dicts(rows, min(st.nrows, cfg.max_outer + 1)))
+
+    def objective_gn(self, g, ip, im, b, params=None, need_grad=True):
+        params = params or ObjectiveParams()
+        mem = self._mem(ip, im, b)
+        grad = self._like(b, g.faces)
+        res = self._like(b, g.cells)
+        ev = ObjectiveEval()
+        self._check(self.lib.epc_objective_gn(self.h, C.byref(g), mem, self._ptr(ip), self._ptr(im),
+                                              self._ptr(b), C.byref(params), int(need_grad),
+                                              C.byref(ev), self._ptr(grad), self._ptr(res)))
+        return dict(value=ev.value, dist=ev.dist, smooth=ev.smooth, pen=ev.pen,
+                    feasible=bool(ev.feasible), grad=grad, residual=res)
+
+    def gn_hessian_build(self, g, ip, im, b, params=None):
+        params = params or ObjectiveParams()
+        mem = self._mem(ip, im, b)
+        d, o, pd = (self._like(b, g.faces) for _ in range(3))
+        self._check(self.lib.epc_gn_hessian_build(self.h, C.byref(g), mem, self._ptr(ip),
+                                                  self._ptr(im), self._ptr(b), C.byref(params),
+                                                  self._ptr(d), self._ptr(o), self._ptr(pd)))
+        return dict(diag=d, off=o, pdiag=pd)
+
+    def gn_hessian_apply(self, g, ip, im, b, x, params=None):
+        params = params or ObjectiveParams()
+        mem = self._mem(ip, im, b, x)
+        y = self._like(b, g.faces)
+        self._check(self.lib.epc_gn_hessian_apply(self.h, C.byref(g), mem, self._ptr(ip),
+                                                  self._ptr(im), self._ptr(b), C.byref(params),
+                                                  self._ptr(x), self._ptr(y)))
+        return y
+
+    def precond_apply(self, g, ip, im, b, kind, r, params=None):
+        params = params or ObjectiveParams()
+        mem = self._mem(ip, im, b, r)
+        z = self._like(b, g.faces)
+        self._check(self.lib.epc_precond_apply(self.h, C.byref(g), mem, self._ptr(ip),
+                                               self._ptr(im), self._ptr(b), C.byref(params), kind,
+                                               self._ptr(r), self._ptr(z)))
+        return z
+
+    def pcg(self, g, ip, im, b, grad, eta, max_iters, kind=abi.PRECOND_BLOCK_JACOBI, params=None):
+        params = params or ObjectiveParams()
+        mem = self._mem(ip, im, b, grad)
+        d = self._like(b, g.faces)
+        res = PcgResult()
+        self._check(self.lib.epc_pcg(self.h, C.byref(g), mem, self._ptr(ip), self._ptr(im),
+                                     self._ptr(b), C.byref(params), kind, self._ptr(grad), eta,
+                                     max_iters, self._ptr(d), C.byref(res)))
+        return dict(d=d, iters=res.iters, relres=res.relres, relres_prec=res.relres_prec,
+                    reached_tol=bool(res.reached_tol))
+
+
+_default = None
+
+
+def context(device=0):
+    global _default
+    if _default is None:
+        _default = Context(device)
+    return _default

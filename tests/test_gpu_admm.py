@@ -1,0 +1,143 @@
+"""ADMM hot path on the GPU vs the oracle (the C restatement of the
+reference, bitwise pinned to it): b-step, z-step, dual update, the full
+admm_solve loop, and batched column QPs. All through the C ABI."""
+import numpy as np
+import pytest
+
+from paper_1607_00531_b200 import abi, synth
+
+pytestmark = pytest.mark.gpu
+
+EXACT = dict(eps_abs=1e-300, eps_rel=1e-300)
+
+
+def small_pair(m=(16, 12, 8), seed=7, scale=1.0):
+    d = synth.make_pair(synth.SynthSpec(m=m, seed=seed))
+    return d.grid, d.iplus * scale, d.iminus * scale
+
+
+def state_after(oracle, g, ip, im, iters, scale_cfg=None):
+    cfg = abi.AdmmConfig(max_iter=iters, **EXACT)
+    r = oracle.admm_solve(g, ip, im, cfg=cfg)
+    return r
+
+
+@pytest.mark.parametrize("scale", [1.0, 400.0])
+def test_b_update_bitwise(ctx, oracle, scale):
+    g, ip, im = small_pair(scale=scale)
+    st = state_after(oracle, g, ip, im, 6)
+    for rho in (st["rho"], 1e6, 100.0):
+        ref = oracle.b_update(g, ip, im, st["b"], st["z"], st["u"], rho)
+        out = ctx.b_update(g, ip, im, st["b"], st["z"], st["u"], rho)
+        assert ref["rc"] == 0
+        assert np.array_equal(out["b"], ref["b"]), np.abs(out["b"] - ref["b"]).max()
+        assert out["sqp_iters"] == ref["sqp_iters"]
+        assert out["qp_iters"] == ref["qp_iters"]
+        assert out["kkt_violation"] == ref["kkt_violation"]
+
+
+def test_z_update_bitwise(ctx, oracle):
+    g, ip, im = small_pair()
+    rng = np.random.default_rng(3)
+    b, u = rng.uniform(-1, 1, g.faces), rng.uniform(-1, 1, g.faces)
+    for rho, alpha in ((3.0, 7.0), (1e6, 50.0), (100.0, 50.0)):
+        ref = oracle.z_update(g, b, u, rho, alpha)
+        out = ctx.z_update(g, b, u, rho, alpha)
+        assert np.array_equal(out, ref), np.abs(out - ref).max()
+
+
+def test_z_update_2d_and_anisotropic(ctx, oracle):
+    rng = np.random.default_rng(4)
+    for g in (abi.Grid.make(6, 5, 4, h=(0.5, 1.0, 1.5)), abi.Grid.make(12, 10, 1),
+              abi.Grid.make(7, 33, 19, h=(1.0, 0.7, 1.3))):
+        b, u = rng.uniform(-1, 1, g.faces), rng.uniform(-1, 1, g.faces)
+        ref = oracle.z_update(g, b, u, 3.0, 7.0)
+        out = ctx.z_update(g, b, u, 3.0, 7.0)
+        assert np.array_equal(out, ref), (g.dims(), np.abs(out - ref).max())
+
+
+def test_dual_update(ctx, oracle):
+    g, _, _ = small_pair()
+    rng = np.random.default_rng(5)
+    b, zn, zo, uo = (rng.uniform(-1, 1, g.faces) for _ in range(4))
+    u_ref, r_ref = oracle.dual_update(g, b, zn, zo, uo, 2.0, 0.2, 0.2)
+    u_out, r_out = ctx.dual_update(g, b, zn, zo, uo, 2.0, 0.2, 0.2)
+    assert np.array_equal(u_out, u_ref)
+    for k in r_ref:
+        assert r_out[k] == pytest.approx(r_ref[k], rel=1e-13)
+
+
+@pytest.mark.parametrize("scale", [1.0, 400.0])
+def test_admm_solve_small_bitwise(ctx, oracle, scale):
+    g, ip, im = small_pair(scale=scale)
+    cfg = abi.AdmmConfig(max_iter=20, **EXACT)
+    ref = oracle.admm_solve(g, ip, im, cfg=cfg)
+    out = ctx.admm_solve(g, ip, im, cfg=cfg)
+    assert out["stop"] == ref["stop"] and len(out["rows"]) == len(ref["rows"])
+    assert np.array_equal(out["b"], ref["b"]), np.abs(out["b"] - ref["b"]).max()
+    assert np.array_equal(out["z"], ref["z"])
+    assert np.array_equal(out["u"], ref["u"])
+    assert out["rho"] == ref["rho"]
+    for a, r in zip(out["rows"], ref["rows"]):
+        assert a["rho"] == r["rho"]
+        assert a["kkt_violation"] == r["kkt_violation"]
+        for k in ("primal_res", "dual_res", "eps_pri", "eps_dual", "lagrangian"):
+            assert a[k] == pytest.approx(r[k], rel=1e-12, abs=1e-300), k
+
+
+def test_admm_solve_default_tolerances_stop_early(ctx, oracle):
+    g, ip, im = small_pair()
+    ref = oracle.admm_solve(g, ip, im)
+    out = ctx.admm_solve(g, ip, im)
+    assert out["stop"] == ref["stop"]
+    assert len(out["rows"]) == len(ref["rows"])
+    assert np.array_equal(out["b"], ref["b"])
+
+
+def test_qp_batch_matches_oracle(ctx, oracle):
+    rng = np.random.default_rng(77)
+    n, h, nqp = 5, 0.8, 200
+    gd = 2.5 + rng.uniform(-1, 1, (nqp, n))
+    go = np.zeros((nqp, n))
+    go[:, :-1] = 0.9 * rng.uniform(-1, 1, (nqp, n - 1))
+    c = 4.0 * rng.uniform(-1, 1, (nqp, n))
+    x0 = np.zeros((nqp, n))
+    out = ctx.qp_active_set_batch(n, h, gd, go, c, x0, 200)
+    for q in range(nqp):
+        ref = oracle.qp_active_set(n, h, gd[q].copy(), go[q].copy(), c[q].copy(), x0[q].copy(), 200)
+        assert out["status"][q] == ref["rc"] == 0
+        assert np.array_equal(out["x"][q], ref["x"])
+        assert np.array_equal(out["lam"][q], ref["lam"])
+        assert np.array_equal(out["sign"][q], ref["sign"])
+        assert out["iters"][q] == ref["iters"]
+        kk = oracle.verify_qp_kkt(n, h, gd[q].copy(), go[q].copy(), c[q].copy(), ref["x"], ref["lam"], ref["sign"])
+        assert out["kkt"][q] == kk
+
+
+def test_qp_goldens(ctx):
+    # test_admm.cpp:101-124: unconstrained optimum [3,-3] clamps to [0.5,-0.5], lambda 2.5
+    out = ctx.qp_active_set_batch(2, 1.0, [1, 1], [0, 0], [-3, 3], [0, 0], 50)
+    assert out["x"][0] == pytest.approx([0.5, -0.5], rel=1e-12)
+    assert out["sign"][0][0] == 1
+    assert out["lam"][0][0] == pytest.approx(2.5, rel=1e-12)
+    assert out["kkt"][0] <= 1e-10
+    # infeasible start is rejected (std::invalid_argument)
+    out = ctx.qp_active_set_batch(2, 1.0, [1, 1], [0, 0], [0, 0], [0, 5.0], 50)
+    assert out["status"][0] == abi.EPC_ERR_INVALID_ARGUMENT
+    # cycling guard trips at the cap (test_admm.cpp:149-153)
+    out = ctx.qp_active_set_batch(3, 1.0, [1, 1, 1], [0, 0, 0], [-9, 0, 9], [0, 0, 0], 1)
+    assert out["status"][0] == abi.EPC_ERR_RUNTIME
+    assert "cycling guard" in out["message"]
+
+
+@pytest.mark.slow
+def test_admm_c1_bitwise(ctx, oracle):
+    d = synth.make_config("C1")
+    cfg = abi.AdmmConfig(max_iter=50, **EXACT)
+    ref = oracle.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
+    out = ctx.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
+    rel = np.linalg.norm(out["b"] - ref["b"]) / np.linalg.norm(ref["b"])
+    assert rel <= 1e-8
+    assert np.array_equal(out["b"], ref["b"])
+    for a, r in zip(out["rows"], ref["rows"]):
+        assert a["lagrangian"] == pytest.approx(r["lagrangian"], rel=1e-9)
