@@ -96,6 +96,7 @@ enum Slot {
     S_COLI, S_COLD, S_QBUF, S_SBUF, S_PART, S_PART2, S_SCAL, S_PAIR, S_MATS, S_CNT,
     S_TMP0, S_TMP1, S_TMP2, S_TMP3,
     S_GN0, S_GN1, S_GN2, S_GN3, S_GN4, S_GN5, S_GN6, S_GN7, S_GN8, S_GN9,
+    S_X0, S_X1, S_X2, S_X3,
     S_COUNT
 };
 
@@ -1159,4 +1160,6 @@ const char* epc_build_info(void) {
 }
 
 }  // extern "C"
+
+#include "gn_host.inc"
 

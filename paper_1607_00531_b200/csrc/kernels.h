@@ -106,8 +106,55 @@ __global__ void k_dual_standalone(const double* b, const double* zn, const doubl
                                   const double* uo, double* un, long long n, double* partials);
 
 // ---- GN (gn.cu) -------------------------------------------------------------
-struct GnGeom {
-    int m1, n1, m2, m3, dim;
-    long long ncol, ncell, nface;
-    double h1, h2, h3, o1, V;
+struct GnCellArgs {
+    const double *ip, *im, *b;
+    int m1, n1;
+    long long ncell;
+    HDiv dh;
+    double o1, V, beta;
+    double *r, *jlo, *jhi, *dphi, *phi2;  // outputs (cells), any may be null except as needed
+    double* partials;                      // per block: {r^2, (D1b)^2, phi, max|D1b|}
 };
+struct GnFaceArgs {
+    const double *b, *r, *jlo, *jhi, *dphi, *dir;
+    int m1, n1, m2, m3;
+    long long nface;
+    double V, alpha, beta, w1, w2, w3, ih2, ih3;
+    double* grad;      // null: sums only
+    double* partials;  // per block: {(D2b)^2, (D3b)^2, grad.dir}
+};
+struct GnHessArgs {
+    const double *jlo, *jhi, *phi2;
+    int m1, n1, m2, m3, dim;
+    long long nface;
+    double V, wl, wp, gamma, beta, w2, w3;
+    double *diag, *off, *pdiag;
+};
+struct GnHvArgs {
+    const double *diag, *off, *z, *p_old;
+    double *p_new, *y;
+    int mode;  // 0: p = z, 1: p = z + beta p_old, 2: p = p_old
+    double beta, w2, w3;
+    int m1, n1, m2, m3;
+    long long nface;
+    double* partials;
+};
+struct GnUpdArgs {
+    double *d, *r, *z;
+    const double *p, *q, *fd, *fl, *pdiag;
+    double a, ma;
+    int do_axpy, kind, n1;
+    long long ncol;
+    double* partials;  // per block {r.r, r.z}
+};
+__global__ void k_gn_cells(GnCellArgs A);
+__global__ void k_gn_faces(GnFaceArgs A);
+__global__ void k_gn_hess(GnHessArgs A);
+__global__ void k_gn_factor(const double* pdiag, const double* off, double* fd, double* fl, int n1,
+                            long long ncol, int* col_err);
+__global__ void k_gn_hv(GnHvArgs A);
+__global__ void k_gn_update_prec(GnUpdArgs A);
+__global__ void k_axpy_point(const double* x, const double* d, double t, double* y, long long n);
+__global__ void k_neg_norm(const double* g, double* r, long long n, double* partials);
+__global__ void k_dot2(const double* a, const double* b, long long n, double* partials);
+__global__ void k_gn_copy(const double* src, double* dst, long long n);
