@@ -339,10 +339,12 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
     const long long total = g.ncol * npairs;
     const size_t smem = bstep_smem_bytes(g.n1);
     if (smem > ctx->smem_optin) fail(EPC_ERR_UNSUPPORTED, "column too long for shared memory");
-    CK(cudaFuncSetAttribute(k_admm_bstep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const HDiv hd = make_hdiv(g.h1);
+    void (*kern)(BStepParams) = hd.pow2 ? k_admm_bstep_t<HPow2> : k_admm_bstep_t<HGen>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)ctx->smem_optin));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_admm_bstep, 32, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem));
     if (per_sm < 1) fail(EPC_ERR_UNSUPPORTED, "b-step kernel does not fit on an SM");
     const long long slots = std::min<long long>((long long)ctx->num_sms * per_sm, total);
     const int qcap = g.m1;
@@ -383,11 +385,16 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
     P.col_fd = col_d + 2 * total;
     P.qbuf = qbuf;
     P.sbuf = sbuf;
+    P.wbuf = slot_t<double>(ctx, S_X1, (size_t)slots * 2 * g.n1);
     P.qcap = qcap;
     P.counter = cnt;
     P.total_cols = total;
     P.timing = (ctx->mode & EPC_MODE_BSTEP_TIMING) ? slot_t<long long>(ctx, S_GN9, 16) : nullptr;
-    EPC_LAUNCH(ctx, "admm_bstep", k_admm_bstep, (unsigned)slots, 32, smem, P);
+    // line-search speculation (mode bits 8-11: trials per pass, bit 12: inline)
+    const int lk = (ctx->mode >> 8) & 15;
+    P.ls_k = lk ? lk : 2;
+    P.ls_inline = (ctx->mode >> 12) & 1;
+    EPC_LAUNCH(ctx, "admm_bstep", kern, (unsigned)slots, 32, smem, P);
     check_launch();
     return BStepRun{col_i, col_d};
 }
@@ -572,7 +579,7 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
             za.active = batch ? act_dev : nullptr;
             za.alpha = p->alpha;
             run_zstep(ctx, g, npairs, M, za);
-            const int nbz = 64;
+            const int nbz = (int)std::min<long long>(g.ncol, (long long)ctx->num_sms * 4);
             double* zp = slot_t<double>(ctx, S_PART2, (size_t)npairs * nbz * 2);
             EPC_LAUNCH(ctx, "zdiff_sums", k_zdiff_sums, dim3(nbz, npairs), 256, 0, Z[1], g.nface,
                        g.n1, g.m2, g.m3, 1.0 / g.h2, 1.0 / g.h3, zp);
@@ -1117,6 +1124,7 @@ int epc_qp_active_set_batch(epc_context* ctx, int nqp, int n, double h, const do
         P.kkt = dk;
         P.qbuf = slot_t<double>(ctx, S_QBUF, (size_t)blocks * qcap * n);
         P.sbuf = slot_t<double>(ctx, S_SBUF, (size_t)blocks * qcap * qcap);
+        P.wbuf = slot_t<double>(ctx, S_X2, (size_t)blocks * 2 * n);
         P.qcap = qcap;
         EPC_LAUNCH(ctx, "qp_batch", k_qp_batch, blocks, 32, smem, P);
         check_launch();

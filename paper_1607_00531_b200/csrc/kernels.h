@@ -20,13 +20,16 @@ struct BStepParams {
     int check_kkt, qp_cap;
     int *col_err, *col_sqp, *col_qp, *col_maxact;
     double *col_kkt, *col_fr, *col_fd;
-    double *qbuf, *sbuf;
+    double *qbuf, *sbuf, *wbuf;  // per-warp scratch: q rows, Schur, {gradient, multipliers}
     int qcap;
     unsigned long long* counter;
     long long total_cols;
     long long* timing;  // optional [10] phase cycle totals (lane 0), nullptr = off
+    int ls_k;           // concurrent backtracking trials per pass (1 = sequential)
+    int ls_inline;      // 1: up to 7 trials with inline d/e chains; 0: <= 2 precomputed
 };
-__global__ void k_admm_bstep(BStepParams P);
+template <class DH>
+__global__ void k_admm_bstep_t(BStepParams P);  // DH = HPow2 | HGen (model.cuh)
 
 struct QpBatchParams {
     int nqp, n;
@@ -37,7 +40,7 @@ struct QpBatchParams {
     int *sign, *iters;
     double* kkt;
     int* status;
-    double *qbuf, *sbuf;
+    double *qbuf, *sbuf, *wbuf;
     int qcap;
 };
 __global__ void k_qp_batch(QpBatchParams P);

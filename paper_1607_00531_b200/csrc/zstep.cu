@@ -195,19 +195,24 @@ __global__ void __launch_bounds__(256) k_zdiff_sums(const double* z, long long n
     const int pair = blockIdx.y;
     const double* zp = z + (long long)pair * nface;
     const long long layer = (long long)n1 * m2;
+    const int ncol = m2 * m3;
     double s2 = 0.0, s3 = 0.0;
-    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < nface;
-         f += (long long)gridDim.x * blockDim.x) {
-        const long long c = f / n1;
-        const int j = (int)(c % m2), k = (int)(c / m2);
-        const double zf = zp[f];
-        if (j + 1 < m2) {
-            const double o = (zp[f + n1] - zf) * ih2;
-            s2 += o * o;
-        }
-        if (m3 > 1 && k + 1 < m3) {
-            const double o = (zp[f + layer] - zf) * ih3;
-            s3 += o * o;
+    // block per column range, threads along the contiguous column (coalesced,
+    // no 64-bit index division per element)
+    for (int c = blockIdx.x; c < ncol; c += gridDim.x) {
+        const int j = c % m2, k = c / m2;
+        const double* zc = zp + (long long)c * n1;
+        const bool hj = j + 1 < m2, hk = m3 > 1 && k + 1 < m3;
+        for (int i = threadIdx.x; i < n1; i += blockDim.x) {
+            const double zf = zc[i];
+            if (hj) {
+                const double o = (zc[i + n1] - zf) * ih2;
+                s2 += o * o;
+            }
+            if (hk) {
+                const double o = (zc[i + layer] - zf) * ih3;
+                s3 += o * o;
+            }
         }
     }
     const double t2 = block_sum(s2, sh);
