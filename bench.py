@@ -178,36 +178,47 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     ctx = Context(local, stream=stream)
 
-    # each rank: its own volume pair (replica) of the config
-    spec = synth.CONFIGS[a.config]
     from dataclasses import replace
-    spec = replace(spec, scale=a.scale, seed=spec.seed + 1000 * rank)
-    d = synth.make_pair(spec)
-    g = d.grid
-    ip_d = torch.from_numpy(d.iplus).to(dev)
-    im_d = torch.from_numpy(d.iminus).to(dev)
-    ip_h = torch.from_numpy(d.iplus).pin_memory()
-    im_h = torch.from_numpy(d.iminus).pin_memory()
-    bo_h = torch.empty(g.faces, dtype=torch.float64).pin_memory()
-    zo_h = torch.empty(g.faces, dtype=torch.float64).pin_memory()
-    uo_h = torch.empty(g.faces, dtype=torch.float64).pin_memory()
+
+    from paper_1607_00531_b200 import shard
     cfg = abi.AdmmConfig(max_iter=iters, eps_abs=1e-300, eps_rel=1e-300)
+    if a.config == "C4":
+        # 64 independent pairs sharded across ranks (no data-path collective)
+        total_pairs = 64
+        first, npairs = shard.shard_range(total_pairs, rank, world)
+        g, ipn, imn = synth.make_batch("C4", npairs=npairs, first=first, scale=a.scale)
+    else:
+        # each rank: its own volume pair (replica) of the config
+        spec = synth.CONFIGS[a.config]
+        spec = replace(spec, scale=a.scale, seed=spec.seed + 1000 * rank)
+        d = synth.make_pair(spec)
+        g, ipn, imn = d.grid, d.iplus, d.iminus
+        total_pairs, npairs = world, 1
+    ip_d = torch.from_numpy(ipn).to(dev)
+    im_d = torch.from_numpy(imn).to(dev)
+    ip_h = torch.from_numpy(ipn).pin_memory()
+    im_h = torch.from_numpy(imn).pin_memory()
+    bo_h = torch.empty(g.faces * npairs, dtype=torch.float64).pin_memory()
+    zo_h = torch.empty(g.faces * npairs, dtype=torch.float64).pin_memory()
+    uo_h = torch.empty(g.faces * npairs, dtype=torch.float64).pin_memory()
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
     def solve_device():
-        return ctx.admm_solve(g, ip_d, im_d, cfg=cfg)
+        if npairs == 1 and a.config != "C4":
+            return ctx.admm_solve(g, ip_d, im_d, cfg=cfg)
+        return ctx.admm_solve_batch(g, npairs, ip_d, im_d, cfg=cfg)
 
     def solve_host():
         # C ABI with pinned host buffers: H2D of I+/I-, D2H of b, z, u inside the call
         import ctypes as C
-        rows = (abi.AdmmRow * iters)()
-        st = abi.SolveStatus()
-        rho = C.c_double(0.0)
+        rows = (abi.AdmmRow * (iters * npairs))()
+        st = (abi.SolveStatus * npairs)()
+        rho = (C.c_double * npairs)()
         P = lambda t: C.c_void_p(t.data_ptr())
-        rc = ctx.lib.epc_admm_solve(ctx.h, C.byref(g), abi.EPC_MEM_HOST, P(ip_h), P(im_h), None,
-                                    None, None, P(bo_h), P(zo_h), P(uo_h), C.byref(rho),
-                                    C.byref(abi.ObjectiveParams()), C.byref(cfg), 0, rows, iters,
-                                    C.byref(st))
+        rc = ctx.lib.epc_admm_solve_batch(ctx.h, C.byref(g), npairs, abi.EPC_MEM_HOST, P(ip_h),
+                                          P(im_h), None, None, None, P(bo_h), P(zo_h), P(uo_h),
+                                          rho, C.byref(abi.ObjectiveParams()), C.byref(cfg), 0,
+                                          rows, iters, st)
         assert rc == 0, ctx._err()
         return st
 
@@ -249,7 +260,7 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     faces_iters = g.faces * iters
-    value = faces_iters * world * a.steps / t_max
+    value = faces_iters * total_pairs * a.steps / t_max
 
     # e2e through the C ABI with pinned host buffers
     solve_host()
@@ -259,7 +270,7 @@ def main():
         tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt.item())
-    e2e = faces_iters * world * a.steps / t_e2e
+    e2e = faces_iters * total_pairs * a.steps / t_e2e
 
     # roofline: per-kernel CUDA-event timing of one profiled solve
     ctx.profile(True)
@@ -299,7 +310,9 @@ def main():
     cpu = None
     if rank == 0 and not a.no_cpu_baseline:
         try:
-            kind, dt, cores = cpu_reference(d, a.ref_iters, os.cpu_count() or 1)
+            one = synth.VolumePairData(g, np.ascontiguousarray(ipn[:g.cells]),
+                                       np.ascontiguousarray(imn[:g.cells]), None)
+            kind, dt, cores = cpu_reference(one, a.ref_iters, os.cpu_count() or 1)
             cpu = {"value": g.faces * a.ref_iters / dt, "unit": UNIT, "cores": cores, "kind": kind,
                    "sample": f"{a.ref_iters} ADMM iterations of the {a.config} solve"}
         except Exception as e:  # the checker is optional on a bench box
@@ -314,11 +327,13 @@ def main():
                 "config": {"workload": f"ADMM {a.config} {'x'.join(map(str, g.dims()))}, "
                                        f"{iters} iterations, fp64, from b=0",
                            "faces": g.faces, "iterations": iters, "intensity_scale": a.scale,
-                           "parallelism": f"replicas x{world}",
+                           "pairs": total_pairs,
+                           "parallelism": (f"pairs sharded {total_pairs}/{world} ranks"
+                                           if a.config == "C4" else f"replicas x{world}"),
                            "l2": "256 MB flush write before every timed step; working set > L2",
                            "time_to_solution_s": t_max / a.steps},
-                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * nc * 8,
-                        "d2h_bytes_per_step": 3 * nf * 8},
+                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * nc * 8 * npairs,
+                        "d2h_bytes_per_step": 3 * nf * 8 * npairs},
                 "gpu_launches": launches, "clocks": clk.summary(),
                 "roofline": roofline, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
