@@ -150,6 +150,36 @@ struct GnUpdArgs {
     long long ncol;
     double* partials;  // per block {r.r, r.z}
 };
+// ---- device-resident PCG (pcg.cu) ---------------------------------------------
+struct PcgState {
+    int done, err, iters, reached, max_iters;
+    unsigned int cnt;  // last-block ticket, reset by the last block
+    double rz, alpha, beta, gnorm, prec0, relres, relres_prec, eta;
+};
+struct PcgHvArgs {
+    const double *diag, *off, *z, *p_old;
+    double *p_new, *q;
+    double w2, w3;
+    int m1, n1, m2, m3, ncol;
+    double* partials;
+};
+struct PcgUpdArgs {
+    double *d, *r, *z;
+    const double *p, *q, *fd, *fl, *pdiag;
+    int phase, kind, n1;
+    long long ncol;
+    double* partials;
+    int cpw;  // reserved (columns per warp), 1
+};
+__global__ void k_pcg_start(const double* g, double* r, double* d, long long n, double* partials,
+                            PcgState* S);
+__global__ void k_pcg_hv(PcgHvArgs A, PcgState* S);
+__global__ void k_pcg_p(const double* __restrict__ z, const double* __restrict__ p_old,
+                        double* __restrict__ p_new, long long n, const PcgState* S);
+__global__ void k_vec_differs(const double* a, const double* b, long long n, int* flag);
+__global__ void k_first_error(const int* col_err, long long ncol, int* out);
+__global__ void k_pcg_update(PcgUpdArgs A, PcgState* S);
+
 __global__ void k_gn_cells(GnCellArgs A);
 __global__ void k_gn_faces(GnFaceArgs A);
 __global__ void k_gn_hess(GnHessArgs A);

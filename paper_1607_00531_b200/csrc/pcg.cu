@@ -1,0 +1,334 @@
+// pcg.cu — device-resident PCG loop for GN (pcg, proj/src/gn_pcg.cpp:92-131).
+//
+// The loop scalars (rz, p.q, alpha, beta, relres) never leave the device:
+// each kernel reduces its per-block partials in a fixed order in the last
+// block to finish (threadfence + atomic ticket; deterministic), then applies
+// the reference's scalar update. The host enqueues iterations in chunks and
+// reads the state once per chunk; kernels of iterations after convergence
+// (or after a curvature failure) return immediately.
+//
+// Per iteration: k_pcg_hv (p = z + beta p; q = H p; p.q; alpha = rz / pq)
+// and k_pcg_update (d += alpha p; r += (-alpha) q; z = M^{-1} r; r.r, r.z;
+// relres, relres_prec, stop test, beta = rz_new / rz). Element-wise work is
+// bitwise the reference's; the sweeps of the block-Jacobi solve run on lane
+// 0 from shared memory with the divisions lane-parallel in between.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+// Fixed-order sum of n partials by one block; result valid in thread 0.
+// Four independent accumulators per thread keep several L2 loads in flight
+// (the last block runs alone, so its latency is on the critical path).
+__device__ double last_block_sum(const double* part, int n, int stride, int off, double* sh) {
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    const int bd = blockDim.x;
+    int b = threadIdx.x;
+    for (; b + 3 * bd < n; b += 4 * bd) {
+        v0 += __ldcg(part + (size_t)b * stride + off);
+        v1 += __ldcg(part + (size_t)(b + bd) * stride + off);
+        v2 += __ldcg(part + (size_t)(b + 2 * bd) * stride + off);
+        v3 += __ldcg(part + (size_t)(b + 3 * bd) * stride + off);
+    }
+    for (; b < n; b += bd) v0 += __ldcg(part + (size_t)b * stride + off);
+    return block_sum((v0 + v1) + (v2 + v3), sh);
+}
+
+// Returns true in every thread of the last block to arrive.
+__device__ bool arrive_last(unsigned int* counter) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int t = atomicAdd(counter, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    return last;
+}
+
+// TridiagFactor::solve_column (operators.cpp:248-255) on lane 0 / all lanes:
+// forward sweep, lane-parallel divisions, backward sweep. Restrict-qualified
+// so the compiler hoists the independent loads ahead of the chain.
+// Forward / backward sweeps with the operands of the next 4 steps loaded
+// while the current 4 run (two register banks, no rotation moves): fewer
+// issued instructions per step than the generic helpers, which matters
+// because these single-lane chains are issue-bound with many warps per SMSP.
+__device__ __forceinline__ void fwd4(double* __restrict__ v, const double* __restrict__ l, int n) {
+    double prev = v[0];
+    int i = 1;
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+    if (i + 4 <= n) {
+        a0 = l[0]; a1 = l[1]; a2 = l[2]; a3 = l[3];
+        b0 = v[1]; b1 = v[2]; b2 = v[3]; b3 = v[4];
+    }
+    for (; i + 4 <= n; i += 4) {
+        double c0 = 0, c1 = 0, c2 = 0, c3 = 0, e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+        if (i + 8 <= n) {
+            c0 = l[i + 3]; c1 = l[i + 4]; c2 = l[i + 5]; c3 = l[i + 6];
+            e0 = v[i + 4]; e1 = v[i + 5]; e2 = v[i + 6]; e3 = v[i + 7];
+        }
+        prev = b0 - a0 * prev; v[i] = prev;
+        prev = b1 - a1 * prev; v[i + 1] = prev;
+        prev = b2 - a2 * prev; v[i + 2] = prev;
+        prev = b3 - a3 * prev; v[i + 3] = prev;
+        a0 = c0; a1 = c1; a2 = c2; a3 = c3;
+        b0 = e0; b1 = e1; b2 = e2; b3 = e3;
+    }
+    for (; i < n; ++i) {
+        prev = v[i] - l[i - 1] * prev;
+        v[i] = prev;
+    }
+}
+
+__device__ __forceinline__ void bwd4(double* __restrict__ v, const double* __restrict__ l, int n) {
+    double nxt = v[n - 1];
+    int i = n - 2;
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+    if (i - 3 >= 0) {
+        a0 = l[i]; a1 = l[i - 1]; a2 = l[i - 2]; a3 = l[i - 3];
+        b0 = v[i]; b1 = v[i - 1]; b2 = v[i - 2]; b3 = v[i - 3];
+    }
+    for (; i - 3 >= 0; i -= 4) {
+        double c0 = 0, c1 = 0, c2 = 0, c3 = 0, e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+        if (i - 7 >= 0) {
+            c0 = l[i - 4]; c1 = l[i - 5]; c2 = l[i - 6]; c3 = l[i - 7];
+            e0 = v[i - 4]; e1 = v[i - 5]; e2 = v[i - 6]; e3 = v[i - 7];
+        }
+        nxt = b0 - a0 * nxt; v[i] = nxt;
+        nxt = b1 - a1 * nxt; v[i - 1] = nxt;
+        nxt = b2 - a2 * nxt; v[i - 2] = nxt;
+        nxt = b3 - a3 * nxt; v[i - 3] = nxt;
+        a0 = c0; a1 = c1; a2 = c2; a3 = c3;
+        b0 = e0; b1 = e1; b2 = e2; b3 = e3;
+    }
+    for (; i >= 0; --i) {
+        nxt = v[i] - l[i] * nxt;
+        v[i] = nxt;
+    }
+}
+
+__device__ __forceinline__ void ldlt_solve_warp(double* __restrict__ v, const double* __restrict__ l,
+                                                const double* __restrict__ d, int n) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) fwd4(v, l, n);
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) v[i] = v[i] / d[i];
+    __syncwarp();
+    if (lane == 0) bwd4(v, l, n);
+    __syncwarp();
+}
+
+}  // namespace
+
+// flag = (a != b) anywhere (values compared with ==, like std::vector's !=);
+// the Wolfe driver's re-evaluation test (gn_pcg.cpp:267-269).
+__global__ void k_vec_differs(const double* a, const double* b, long long n, int* flag) {
+    int d = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        d |= !(a[i] == b[i]);
+    if (__any_sync(FULL_MASK, d) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// lowest column with a failed pivot (col_err[c] != 0), or INT_MAX
+__global__ void k_first_error(const int* col_err, long long ncol, int* out) {
+    int m = 0x7fffffff;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < ncol;
+         c += (long long)gridDim.x * blockDim.x)
+        if (col_err[c]) m = min(m, (int)c);
+    m = warp_min_int(m);
+    if ((threadIdx.x & 31) == 0 && m != 0x7fffffff) atomicMin(out, m);
+}
+
+// p_new = z (first iteration) or z + beta p_old (gn_pcg.cpp:128, applied at
+// the top of the next iteration); element-wise.
+__global__ void __launch_bounds__(256) k_pcg_p(const double* __restrict__ z,
+                                              const double* __restrict__ p_old,
+                                              double* __restrict__ p_new, long long n,
+                                              const PcgState* S) {
+    if (S->done) return;
+    const bool first = S->iters == 0;
+    const double beta = S->beta;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        p_new[i] = first ? z[i] : z[i] + beta * p_old[i];
+}
+
+// r = -g; gnorm = ||g||; zero-gradient short circuit (gn_pcg.cpp:96-103).
+__global__ void __launch_bounds__(256) k_pcg_start(const double* g, double* r, double* d,
+                                                  long long n, double* partials, PcgState* S) {
+    __shared__ double sh[8];
+    double s = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double v = g[i];
+        r[i] = -v;
+        d[i] = 0.0;
+        s += v * v;
+    }
+    const double t = block_sum(s, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = t;
+    if (arrive_last(&S->cnt)) {
+        __syncthreads();
+        const double gg = last_block_sum(partials, gridDim.x, 1, 0, sh);
+        if (threadIdx.x == 0) {
+            const double gnorm = sqrt(gg);
+            S->gnorm = gnorm;
+            S->iters = 0;
+            S->err = 0;
+            S->reached = 0;
+            S->done = gnorm == 0.0 ? 1 : 0;
+            if (gnorm == 0.0) S->reached = 1;
+            S->cnt = 0;
+        }
+    }
+}
+
+// q = H p with p = z (first iteration) or z + beta p_old, written to p_new;
+// partial p.q; the last block forms alpha = rz / pq (gn_pcg.cpp:110-114).
+// One block per column (j,k), threads along the contiguous column.
+__global__ void __launch_bounds__(128) k_pcg_hv(PcgHvArgs A, PcgState* S) {
+    __shared__ double sh[8];
+    if (S->done) return;
+    const int n1 = A.n1, m1 = A.m1, m2 = A.m2, m3 = A.m3;
+    const long long layer = (long long)n1 * m2;
+    const double* __restrict__ P = A.p_new;  // written by k_pcg_p
+    const double* __restrict__ D = A.diag;
+    const double* __restrict__ O = A.off;
+    double s = 0.0;
+    for (int c = blockIdx.x; c < A.ncol; c += gridDim.x) {
+        const int j = c % m2, k = c / m2;
+        const long long base = (long long)c * n1;
+        for (int i = threadIdx.x; i < n1; i += blockDim.x) {
+            const long long f = base + i;
+            const double x = P[f];
+            double acc = D[f] * x;
+            if (i > 0) acc += O[f - 1] * P[f - 1];
+            if (i < m1) acc += O[f] * P[f + 1];
+            double y = acc;
+            if (j > 0) y += A.w2 * (x - P[f - n1]);
+            if (j + 1 < m2) y += A.w2 * (x - P[f + n1]);
+            if (m3 > 1) {
+                if (k > 0) y += A.w3 * (x - P[f - layer]);
+                if (k + 1 < m3) y += A.w3 * (x - P[f + layer]);
+            }
+            A.q[f] = y;
+            s += x * y;
+        }
+    }
+    const double t = block_sum(s, sh);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = t;
+    if (arrive_last(&S->cnt)) {
+        __syncthreads();
+        const double pq = last_block_sum(A.partials, gridDim.x, 1, 0, sh);
+        if (threadIdx.x == 0) {
+            if (!(pq > 0.0)) {
+                S->err = 1;  // "pcg: nonpositive curvature encountered"
+                S->done = 1;
+            } else {
+                S->alpha = S->rz / pq;
+            }
+            S->cnt = 0;
+        }
+    }
+}
+
+// d += alpha p; r += (-alpha) q (phase 1) then z = M^{-1} r and the partial
+// sums r.r, r.z; the last block finishes the iteration (gn_pcg.cpp:115-129).
+// phase 0 (start): no axpys; sets rz and prec0 (gn_pcg.cpp:105-108).
+// One warp per column; r, fd, fl staged in shared memory for the sweeps.
+__global__ void __launch_bounds__(128) k_pcg_update(PcgUpdArgs A, PcgState* S) {
+    extern __shared__ __align__(16) double usm[];
+    __shared__ double red[2][4];
+    __shared__ double sh[8];
+    if (S->done) return;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int n1 = A.n1;
+    const int wpb = blockDim.x >> 5;
+    double* sv = usm + (size_t)wib * 3 * n1;
+    double* sd = sv + n1;
+    double* sl = sd + n1;
+    const double a = S->alpha, ma = -a;
+    // distinct buffers: restrict lets the unrolled staging batch its loads
+    double* __restrict__ Dv = A.d;
+    double* __restrict__ Rv = A.r;
+    const double* __restrict__ Pv = A.p;
+    const double* __restrict__ Qv = A.q;
+    const double* __restrict__ FD = A.fd;
+    const double* __restrict__ FL = A.fl;
+    const bool upd = A.phase == 1, block = A.kind == EPC_PRECOND_BLOCK_JACOBI;
+    double rr = 0.0, rz = 0.0;
+    for (long long c = (long long)blockIdx.x * wpb + wib; c < A.ncol; c += (long long)gridDim.x * wpb) {
+        const size_t o = (size_t)c * n1;
+#pragma unroll 4
+        for (int i = lane; i < n1; i += 32) {
+            double r = Rv[o + i];
+            if (upd) {
+                Dv[o + i] += a * Pv[o + i];
+                r += ma * Qv[o + i];
+                Rv[o + i] = r;
+            }
+            rr += r * r;
+            sv[i] = r;
+            if (block) {
+                sd[i] = FD[o + i];
+                sl[i] = FL[o + i];
+            }
+        }
+        __syncwarp();
+        if (A.kind == EPC_PRECOND_BLOCK_JACOBI) {
+            ldlt_solve_warp(sv, sl, sd, n1);
+        } else if (A.kind == EPC_PRECOND_JACOBI) {
+            for (int i = lane; i < n1; i += 32) sv[i] = sv[i] / A.pdiag[o + i];
+            __syncwarp();
+        }
+        for (int i = lane; i < n1; i += 32) {
+            const double zz = sv[i];
+            A.z[o + i] = zz;
+            rz += A.r[o + i] * zz;
+        }
+        __syncwarp();
+    }
+    rr = warp_sum(rr);
+    rz = warp_sum(rz);
+    if (lane == 0) {
+        red[0][wib] = rr;
+        red[1][wib] = rz;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double x = 0.0, y = 0.0;
+        for (int w = 0; w < wpb; ++w) {
+            x += red[0][w];
+            y += red[1][w];
+        }
+        A.partials[(size_t)blockIdx.x * 2 + 0] = x;
+        A.partials[(size_t)blockIdx.x * 2 + 1] = y;
+    }
+    if (arrive_last(&S->cnt)) {
+        __syncthreads();
+        const double srr = last_block_sum(A.partials, gridDim.x, 2, 0, sh);
+        __syncthreads();
+        const double srz = last_block_sum(A.partials, gridDim.x, 2, 1, sh);
+        if (threadIdx.x == 0) {
+            if (A.phase == 0) {
+                S->rz = srz;
+                S->prec0 = sqrt((srz < 0.0) ? 0.0 : srz);  // sqrt(std::max(rz, 0.0))
+            } else {
+                S->iters += 1;
+                S->relres = sqrt(srr) / S->gnorm;
+                S->relres_prec = S->prec0 > 0.0 ? sqrt((srz < 0.0) ? 0.0 : srz) / S->prec0 : 0.0;
+                if (S->relres <= S->eta) {
+                    S->reached = 1;
+                    S->done = 1;
+                } else {
+                    S->beta = srz / S->rz;
+                    S->rz = srz;
+                    if (S->iters >= S->max_iters) S->done = 1;
+                }
+            }
+            S->cnt = 0;
+        }
+    }
+}
