@@ -150,12 +150,22 @@ void epc_context_destroy(epc_context* ctx);
 int epc_set_stream(epc_context* ctx, void* stream);
 const char* epc_last_error(const epc_context* ctx);
 /* Bitmask of optional modes, EPC_MODE_*; default 0 (reference-exact). */
-enum { EPC_MODE_BSTEP_TIMING = 1 /* accumulate b-step phase cycles (diagnostic) */ };
+enum {
+    EPC_MODE_BSTEP_TIMING = 1, /* accumulate b-step phase cycles and counters (diagnostic) */
+    /* decide every b-step SQP / line-search test on the reference's sequential
+     * sums instead of certified enclosures (diagnostic; identical results) */
+    EPC_MODE_BSTEP_CHAINED = 1 << 13
+};
 int epc_set_mode(epc_context* ctx, int mode_bits);
 /* Phase cycle totals of the b-step kernel since timing was enabled (lane 0
  * clock64 deltas): model, fval sums, factor, solves, QP rest, KKT, step
  * sums, line search, clamp+store, column fetch. */
 int epc_bstep_timing(epc_context* ctx, long long* out10);
+/* b-step event counters since timing was enabled: line-search trials,
+ * trials an enclosure could not decide, undecided stopping tests, failed
+ * line searches, SQP iterations reaching the line search, exact fval
+ * fallbacks. */
+int epc_bstep_counters(epc_context* ctx, long long* out6);
 /* Per-kernel CUDA-event timing on the context stream (for the roofline). */
 int epc_profile_enable(epc_context* ctx, int on);
 /* Fills up to `cap` entries: name (static string), total ms, launch count. */

@@ -10,7 +10,8 @@ from .abi import (AdmmConfig, AdmmRow, BUpdateStats, DualResult, GnConfig, GnRow
                   ObjectiveEval, ObjectiveParams, PcgResult, SolveStatus, dptr, iptr)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libepicorr_b200.so")
+# EPC_LIB: load another build of the same sources (A/B experiments, scripts/)
+LIB_PATH = os.environ.get("EPC_LIB") or os.path.join(HERE, "libepicorr_b200.so")
 _lock = threading.Lock()
 _lib = None
 
@@ -23,7 +24,7 @@ EXPORTS = [
     "epc_b_update", "epc_z_update", "epc_dct_solve", "epc_dual_update",
     "epc_augmented_lagrangian", "epc_rho_schedule", "epc_qp_active_set_batch", "epc_gn_solve",
     "epc_objective_gn", "epc_gn_hessian_build", "epc_gn_hessian_apply", "epc_precond_apply",
-    "epc_pcg", "epc_residual", "epc_build_info", "epc_bstep_timing",
+    "epc_pcg", "epc_residual", "epc_build_info", "epc_bstep_timing", "epc_bstep_counters",
 ]
 
 
@@ -88,6 +89,7 @@ def _declare(L):
     L.epc_residual.argtypes = [X, G, C.c_int, X, X, X, X]
     L.epc_build_info.restype = C.c_char_p
     L.epc_bstep_timing.argtypes = [X, C.POINTER(C.c_longlong)]
+    L.epc_bstep_counters.argtypes = [X, C.POINTER(C.c_longlong)]
 
 
 def load(build_if_missing=True):

@@ -340,7 +340,16 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
     const size_t smem = bstep_smem_bytes(g.n1);
     if (smem > ctx->smem_optin) fail(EPC_ERR_UNSUPPORTED, "column too long for shared memory");
     const HDiv hd = make_hdiv(g.h1);
-    void (*kern)(BStepParams) = hd.pow2 ? k_admm_bstep_t<HPow2> : k_admm_bstep_t<HGen>;
+    const bool diag = (ctx->mode & (EPC_MODE_BSTEP_TIMING | EPC_MODE_BSTEP_CHAINED)) != 0;
+#ifdef EPC_FORCE_DIAG
+    const bool diag_forced = true;
+#else
+    const bool diag_forced = false;
+#endif
+
+    void (*kern)(BStepParams) =
+        hd.pow2 ? (diag || diag_forced ? k_admm_bstep_t<HPow2, true> : k_admm_bstep_t<HPow2, false>)
+                : (diag || diag_forced ? k_admm_bstep_t<HGen, true> : k_admm_bstep_t<HGen, false>);
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)ctx->smem_optin));
     int per_sm = 0;
@@ -348,7 +357,7 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
     if (per_sm < 1) fail(EPC_ERR_UNSUPPORTED, "b-step kernel does not fit on an SM");
     const long long slots = std::min<long long>((long long)ctx->num_sms * per_sm, total);
     const int qcap = g.m1;
-    double* qbuf = slot_t<double>(ctx, S_QBUF, (size_t)slots * qcap * g.n1);
+    double* qbuf = slot_t<double>(ctx, S_QBUF, (size_t)slots * qrows_stride(qcap, g.n1));
     double* sbuf = slot_t<double>(ctx, S_SBUF, (size_t)slots * qcap * qcap);
     int* col_i = slot_t<int>(ctx, S_COLI, (size_t)total * 4);
     double* col_d = slot_t<double>(ctx, S_COLD, (size_t)total * 3);
@@ -390,10 +399,7 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
     P.counter = cnt;
     P.total_cols = total;
     P.timing = (ctx->mode & EPC_MODE_BSTEP_TIMING) ? slot_t<long long>(ctx, S_GN9, 16) : nullptr;
-    // line-search speculation (mode bits 8-11: trials per pass, bit 12: inline)
-    const int lk = (ctx->mode >> 8) & 15;
-    P.ls_k = lk ? lk : 2;
-    P.ls_inline = (ctx->mode >> 12) & 1;
+    P.cert = (ctx->mode & EPC_MODE_BSTEP_CHAINED) ? 0 : 1;
     EPC_LAUNCH(ctx, "admm_bstep", kern, (unsigned)slots, 32, smem, P);
     check_launch();
     return BStepRun{col_i, col_d};
@@ -873,6 +879,14 @@ int epc_bstep_timing(epc_context* ctx, long long* out10) {
     });
 }
 
+int epc_bstep_counters(epc_context* ctx, long long* out6) {
+    return guarded(ctx, [&] {
+        long long* t = slot_t<long long>(ctx, S_GN9, 16);
+        d2h(ctx, out6, t + 10, 6 * sizeof(long long));
+        sync(ctx);
+    });
+}
+
 int epc_profile_enable(epc_context* ctx, int on) {
     if (!on && ctx->profiling) prof_drain(ctx);
     ctx->profiling = on != 0;
@@ -1122,7 +1136,7 @@ int epc_qp_active_set_batch(epc_context* ctx, int nqp, int n, double h, const do
         P.iters = ds + nl;
         P.status = ds + nl + nqp;
         P.kkt = dk;
-        P.qbuf = slot_t<double>(ctx, S_QBUF, (size_t)blocks * qcap * n);
+        P.qbuf = slot_t<double>(ctx, S_QBUF, (size_t)blocks * qrows_stride(qcap, n));
         P.sbuf = slot_t<double>(ctx, S_SBUF, (size_t)blocks * qcap * qcap);
         P.wbuf = slot_t<double>(ctx, S_X2, (size_t)blocks * 2 * n);
         P.qcap = qcap;

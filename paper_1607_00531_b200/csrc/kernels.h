@@ -24,12 +24,13 @@ struct BStepParams {
     int qcap;
     unsigned long long* counter;
     long long total_cols;
-    long long* timing;  // optional [10] phase cycle totals (lane 0), nullptr = off
-    int ls_k;           // concurrent backtracking trials per pass (1 = sequential)
-    int ls_inline;      // 1: up to 7 trials with inline d/e chains; 0: <= 2 precomputed
+    long long* timing;  // optional [16]: phase cycles [0..9] (lane 0), counters [10..15]
+    int cert;           // 1: decide SQP / line-search tests on certified enclosures
 };
-template <class DH>
-__global__ void k_admm_bstep_t(BStepParams P);  // DH = HPow2 | HGen (model.cuh)
+// DH = HPow2 | HGen (model.cuh); DIAG: phase timing / counters and the
+// chained mode compiled in (diagnostic instantiation, selected by ctx->mode)
+template <class DH, bool DIAG>
+__global__ void k_admm_bstep_t(BStepParams P);
 
 struct QpBatchParams {
     int nqp, n;
@@ -45,6 +46,11 @@ struct QpBatchParams {
 };
 __global__ void k_qp_batch(QpBatchParams P);
 size_t bstep_smem_bytes(int n1);
+// Per-warp q-row scratch: qcap rows of n doubles plus CHAIN_PAD before and
+// after (the chain sweeps read the pads).
+__host__ __device__ inline size_t qrows_stride(int qcap, int n) {
+    return (size_t)qcap * n + 2 * CHAIN_PAD;
+}
 
 // ---- dense DCT z-step (zstep.cu) ------------------------------------------
 // Out[row][col] = sum_k A[row][k] * In[k][col], k ascending, unfused mul/add.

@@ -122,6 +122,16 @@ class Context:
         self._check(self.lib.epc_bstep_timing(self.h, out))
         return dict(zip(self.BSTEP_PHASES, list(out)))
 
+    BSTEP_COUNTERS = ["ls_trials", "ls_undecided", "stop_undecided", "ls_failed", "ls_searches",
+                      "fval_exact"]
+    MODE_BSTEP_TIMING = 1
+    MODE_BSTEP_CHAINED = 1 << 13
+
+    def bstep_counters(self):
+        out = (C.c_longlong * 6)()
+        self._check(self.lib.epc_bstep_counters(self.h, out))
+        return dict(zip(self.BSTEP_COUNTERS, list(out)))
+
     def profile_read(self):
         cap = 64
         names = (C.c_char_p * cap)()

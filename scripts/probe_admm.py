@@ -15,6 +15,7 @@ ap.add_argument("--config", default="C1")
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--check", type=int, default=0, help="oracle iterations to compare (0 = skip)")
+ap.add_argument("--prod", action="store_true", help="production kernel (no phase timing)")
 a = ap.parse_args()
 
 t = time.time()
@@ -23,17 +24,18 @@ print(f"generate {a.config}: {time.time() - t:.2f}s faces={d.grid.faces}", flush
 ctx = Context(0)
 cfg = abi.AdmmConfig(max_iter=a.iters, eps_abs=1e-300, eps_rel=1e-300)
 r = ctx.admm_solve(d.grid, d.iplus, d.iminus, cfg=abi.AdmmConfig(max_iter=2, eps_abs=1e-300, eps_rel=1e-300))
-ctx.set_mode(1)
+ctx.set_mode(0 if a.prod else 1)
 ctx.profile(True)
 ctx.profile_reset()
 t = time.time()
 r = ctx.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
 dt = time.time() - t
 prof = ctx.profile_read()
-tm = ctx.bstep_timing()
-tt = sum(tm.values())
-print("b-step phases (lane-0 cycles, all warps):", {k: f"{100*v/tt:.1f}%" for k, v in tm.items()})
-print("  total Gcycles", tt / 1e9)
+if not a.prod:
+    tm = ctx.bstep_timing()
+    tt = sum(tm.values())
+    print("b-step phases (lane-0 cycles, all warps):", {k: f"{100*v/tt:.1f}%" for k, v in tm.items()})
+    print("  total Gcycles", tt / 1e9)
 ctx.profile(False)
 print(f"admm {a.iters} it: {dt:.3f}s  {dt / a.iters * 1e3:.2f} ms/it  "
       f"{d.grid.faces * a.iters / dt / 1e6:.1f} M face-it/s  stop={r['stop']}", flush=True)
