@@ -164,8 +164,9 @@ int epc_bstep_timing(epc_context* ctx, long long* out10);
 /* b-step event counters since timing was enabled: line-search trials,
  * trials an enclosure could not decide, undecided stopping tests, failed
  * line searches, SQP iterations reaching the line search, exact fval
- * fallbacks. */
-int epc_bstep_counters(epc_context* ctx, long long* out6);
+ * fallbacks, then a histogram of the accepted trial index (0, 1, 2-3, 4-7,
+ * 8-15, 16-31, 32-39) and the failed-search count. */
+int epc_bstep_counters(epc_context* ctx, long long* out14);
 /* Per-kernel CUDA-event timing on the context stream (for the roofline). */
 int epc_profile_enable(epc_context* ctx, int on);
 /* Fills up to `cap` entries: name (static string), total ms, launch count. */

@@ -123,12 +123,13 @@ class Context:
         return dict(zip(self.BSTEP_PHASES, list(out)))
 
     BSTEP_COUNTERS = ["ls_trials", "ls_undecided", "stop_undecided", "ls_failed", "ls_searches",
-                      "fval_exact"]
+                      "fval_exact", "acc0", "acc1", "acc2_3", "acc4_7", "acc8_15", "acc16_31",
+                      "acc32_39", "fail"]
     MODE_BSTEP_TIMING = 1
     MODE_BSTEP_CHAINED = 1 << 13
 
     def bstep_counters(self):
-        out = (C.c_longlong * 6)()
+        out = (C.c_longlong * 14)()
         self._check(self.lib.epc_bstep_counters(self.h, out))
         return dict(zip(self.BSTEP_COUNTERS, list(out)))
 
