@@ -37,7 +37,15 @@ import numpy as np  # noqa: E402
 
 from paper_1607_00531_b200 import abi, synth  # noqa: E402
 
-METRIC = "voxel-iterations/s (ADMM, 256x256x96, fp64)"
+METRIC = "voxel-iterations/s (ADMM, 256x256x96, fp64)"  # BASELINE.json metric (C3)
+
+
+def metric_for(config):
+    """BASELINE's metric string, naming the grid actually run (C3 unless --config)."""
+    if config == "C3":
+        return METRIC
+    spec = synth.CONFIGS[config]
+    return f"voxel-iterations/s (ADMM, {'x'.join(map(str, spec.m))}, fp64)"
 UNIT = "face-iterations/s"
 
 
@@ -55,6 +63,8 @@ def parse():
     return ap.parse_args()
 
 
+# fp64 DADD/DMUL issue rate measured on this pool (profiles/r01_ubench_fp64_tput.log)
+FP64_PEAK_TOPS = 18.3
 DEFAULT_ITERS = {"C1": 50, "C2": 50, "C3": 100, "C4": 50, "C5": 50}
 
 
@@ -150,7 +160,7 @@ def run_reference_arm(a, iters):
             times.append(dt)
     t = float(np.mean(times))
     value = d.grid.faces * a.ref_iters / t
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+    line = {"metric": metric_for(a.config), "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
@@ -290,13 +300,28 @@ def main():
     # writes b; each DCT GEMM reads + writes one face field (rhs GEMM reads b,u).
     alg = {"admm_bstep": 8 * (2 * nc + 4 * nf), "dct_fwd2": 8 * 3 * nf, "dct_fwd3_div": 8 * 2 * nf,
            "dct_inv3": 8 * 2 * nf, "dct_inv2_dual": 8 * 7 * nf}
+    # The DCT GEMMs are fp64-pipe bound: 2*M*K*N unfused mul+add per transform
+    # (exact k order, no FMA), against the measured fp64 issue rate
+    # (scripts/ubench_fp64_tput.cu -> profiles/r01_ubench_fp64_tput.log).
+    m1_, m2_, m3_ = g.m
+    n1_ = m1_ + 1
+    pairs_ = npairs if a.config == "C4" else 1
+    fp64_ops = {"dct_fwd2": 2 * m2_ * m2_ * n1_ * m3_ * pairs_,
+                "dct_inv2_dual": 2 * m2_ * m2_ * n1_ * m3_ * pairs_,
+                "dct_fwd3_div": 2 * m3_ * m3_ * n1_ * m2_ * pairs_,
+                "dct_inv3": 2 * m3_ * m3_ * n1_ * m2_ * pairs_}
+    fp64_peak = float(peaks.get("fp64_tops", FP64_PEAK_TOPS)) * 1e12
     kernels = []
     for name, (ms, n) in prof.items():
         if name in alg and n:
             per = ms / n / 1e3
             gbs = alg[name] / per / 1e9
-            kernels.append({"kernel": name, "ms_per_launch": ms / n, "alg_bytes": alg[name],
-                            "achieved_gbs": gbs, "frac_hbm": gbs / hbm_peak})
+            k = {"kernel": name, "ms_per_launch": ms / n, "alg_bytes": alg[name],
+                 "achieved_gbs": gbs, "frac_hbm": gbs / hbm_peak}
+            if name in fp64_ops:
+                k["fp64_tops"] = fp64_ops[name] / per / 1e12
+                k["frac_fp64"] = fp64_ops[name] / per / fp64_peak
+            kernels.append(k)
     top = max(prof.items(), key=lambda kv: kv[1][0])
     bname, (bms, bn) = top
     b_per = bms / bn / 1e3
@@ -320,7 +345,7 @@ def main():
                    "sample": str(e)[:120]}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        line = {"metric": metric_for(a.config), "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_max / a.steps * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",

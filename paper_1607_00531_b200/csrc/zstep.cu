@@ -25,8 +25,11 @@ constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
 }
 
 template <int PRO, int EPI>
-__global__ void __launch_bounds__(NT) k_dct_gemm(GemmParams p) {
-    __shared__ double As[BK][BM];
+// The dual epilogue needs more registers than the plain ones; capping it to
+// three resident CTAs per SM (<= 85 registers) is faster than two with more
+// registers (measured), the other variants fit three CTAs unforced.
+__global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmParams p) {
+    __shared__ double As[BK][BM + 1];  // +1: the transposing store is conflict-free
     __shared__ double Bs[BK][BN];
     __shared__ double red[(NT / 32) * 6];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
