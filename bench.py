@@ -65,6 +65,7 @@ def parse():
 
 # fp64 DADD/DMUL issue rate measured on this pool (profiles/r01_ubench_fp64_tput.log)
 FP64_PEAK_TOPS = 18.3
+NCU_BSTEP_SUMMARY = "r01e_bstep_ncu.json"  # C3 b-step, one launch, ncu --set full
 DEFAULT_ITERS = {"C1": 50, "C2": 50, "C3": 100, "C4": 50, "C5": 50}
 
 
@@ -326,9 +327,19 @@ def main():
     bname, (bms, bn) = top
     b_per = bms / bn / 1e3
     b_ach = alg.get(bname, 0) / b_per / 1e9
+    # DRAM traffic of one b-step launch from the committed ncu --set full
+    # capture summary (scripts/summarize_ncu.py), bytes per launch
+    traffic, traffic_src = None, None
+    try:
+        cap = json.load(open(os.path.join(ROOT, "profiles", NCU_BSTEP_SUMMARY)))
+        mb = float(cap["dram__bytes_read.sum"][0]) + float(cap["dram__bytes_write.sum"][0])
+        if cap["dram__bytes_read.sum"][1] == "Mbyte":
+            traffic, traffic_src = mb * 1e6, "profiles/" + NCU_BSTEP_SUMMARY
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": bname, "achieved": b_ach, "peak": hbm_peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": b_ach / hbm_peak,
-                "traffic": None, "share_of_step": bms / sum(v[0] for v in prof.values()),
+                "traffic": traffic, "traffic_source": traffic_src, "share_of_step": bms / sum(v[0] for v in prof.values()),
                 "note": "b-step is fp64-latency bound (serial SQP/QP chains), not HBM bound",
                 "kernels": kernels}
 

@@ -1,0 +1,67 @@
+"""Summaries for profiles/ (dev aid):
+  launches <ncu --csv launch list> <out.csv>   per-kernel count / total ms / share
+  capture  <.ncu-rep> <out.json>               key metrics + stall mix of one capture
+"""
+import collections
+import csv
+import json
+import subprocess
+import sys
+
+
+def launches(src, dst):
+    rows = [r for r in csv.reader(open(src)) if r]
+    hdr = next(r for r in rows if "Kernel Name" in r)
+    ik, iv, im = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
+    tot = collections.defaultdict(float)
+    cnt = collections.Counter()
+    unit = hdr.index("Metric Unit")
+    for r in rows[rows.index(hdr) + 1:]:
+        if len(r) <= iv or r[im] != "gpu__time_duration.sum":
+            continue
+        scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0,
+                 "nsecond": 1e-6}.get(r[unit], 1.0)
+        name = r[ik].split("(")[0]
+        tot[name] += float(r[iv].replace(",", "")) * scale
+        cnt[name] += 1
+    s = sum(tot.values())
+    with open(dst, "w") as f:
+        f.write("kernel,launches,total_ms,share\n")
+        for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+            f.write(f"{k},{cnt[k]},{v:.3f},{v / s:.4f}\n")
+
+
+def capture(src, dst):
+    out = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    r = list(csv.reader(out.splitlines()))
+    h, u, v = r[0], r[1], r[2]
+    keys = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum",
+            "dram__bytes_write.sum", "launch__grid_size", "launch__block_size",
+            "launch__registers_per_thread", "launch__occupancy_limit_shared_mem",
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"]
+    d = {}
+    for k in keys:
+        if k in h:
+            i = h.index(k)
+            d[k] = [v[i], u[i]]
+    stalls = {}
+    for i, n in enumerate(h):
+        if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued"):
+            try:
+                x = float(v[i].replace(",", ""))
+            except ValueError:
+                continue
+            if x > 0:
+                stalls[n.replace("smsp__pcsamp_warps_issue_stalled_", "")] = x
+    t = sum(stalls.values()) or 1.0
+    d["stall_mix_pct"] = {k: round(100 * x / t, 1) for k, x in
+                          sorted(stalls.items(), key=lambda kv: -kv[1])}
+    json.dump(d, open(dst, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    {"launches": launches, "capture": capture}[sys.argv[1]](sys.argv[2], sys.argv[3])

@@ -141,3 +141,33 @@ def test_admm_c1_bitwise(ctx, oracle):
     assert np.array_equal(out["b"], ref["b"])
     for a, r in zip(out["rows"], ref["rows"]):
         assert a["lagrangian"] == pytest.approx(r["lagrangian"], rel=1e-9)
+
+
+@pytest.mark.parametrize("scale", [1.0, 400.0])
+def test_bstep_modes_bitwise(ctx, oracle, scale):
+    """The certified-enclosure b-step (default), the diagnostic instantiation
+    with counters, and the all-chains mode all return the reference's b, and
+    their line searches make the same decisions (same trial counts)."""
+    from paper_1607_00531_b200.epicorr import Context
+    g, ip, im = small_pair(scale=scale)
+    st = state_after(oracle, g, ip, im, 4)
+    ref = oracle.b_update(g, ip, im, st["b"], st["z"], st["u"], st["rho"])
+    counters = {}
+    try:
+        for name, bits in (("prod", 0), ("diag", Context.MODE_BSTEP_TIMING),
+                           ("chained", Context.MODE_BSTEP_TIMING | Context.MODE_BSTEP_CHAINED)):
+            ctx.set_mode(0)  # counters reset when timing is switched on
+            ctx.set_mode(bits)
+            out = ctx.b_update(g, ip, im, st["b"], st["z"], st["u"], st["rho"])
+            assert np.array_equal(out["b"], ref["b"]), (name, np.abs(out["b"] - ref["b"]).max())
+            assert out["sqp_iters"] == ref["sqp_iters"] and out["qp_iters"] == ref["qp_iters"]
+            if bits:
+                counters[name] = ctx.bstep_counters()
+    finally:
+        ctx.set_mode(0)
+    d, c = counters["diag"], counters["chained"]
+    assert d["ls_trials"] == c["ls_trials"] and d["ls_searches"] == c["ls_searches"]
+    assert c["ls_undecided"] == 0 and 0 <= d["ls_undecided"] <= d["ls_trials"]
+    hist = sum(d[k] for k in ("acc0", "acc1", "acc2_3", "acc4_7", "acc8_15", "acc16_31",
+                              "acc32_39", "fail"))
+    assert hist == d["ls_searches"]
