@@ -175,11 +175,123 @@ def run_reference_arm(a, iters):
     return 0
 
 
+def run_slabs(a, iters):
+    """C5: one volume, k-slabs across the ranks; strong scaling.
+    Each rank generates the same seeded volume and keeps its slab; the solve
+    is paper_1607_00531_b200.dist_admm over the epc_slab_* C ABI, with NCCL
+    all-to-all transposes, a one-layer halo and a scalar all-gather between
+    the local steps. World size 1 runs the same driver without collectives."""
+    import torch
+    from paper_1607_00531_b200 import dist_admm
+    from paper_1607_00531_b200.epicorr import Context
+    rank, world, local, dist = dist_setup(a.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = Context(local, stream=stream)
+    d = synth.make_config(a.config, scale=a.scale)
+    g = d.grid
+    slabs = dist_admm.Slabs(g.m[0], g.m[1], g.m[2], world)
+    k0, mk = slabs.k_range(rank)
+    cl = g.m[0] * g.m[1]
+    ip_h = torch.from_numpy(np.ascontiguousarray(d.iplus[k0 * cl:(k0 + mk) * cl])).pin_memory()
+    im_h = torch.from_numpy(np.ascontiguousarray(d.iminus[k0 * cl:(k0 + mk) * cl])).pin_memory()
+    ip_d, im_d = ip_h.to(dev), im_h.to(dev)
+    cfg = abi.AdmmConfig(max_iter=iters, eps_abs=1e-300, eps_rel=1e-300)
+    backend = dist_admm.DeviceBackend(ctx, dev)
+    nf = slabs.slab_faces(rank)
+    out_h = [torch.empty(nf, dtype=torch.float64).pin_memory() for _ in range(3)]
+
+    def solve(host):
+        ip_, im_ = (ip_h.to(dev, non_blocking=True), im_h.to(dev, non_blocking=True)) if host \
+            else (ip_d, im_d)
+        torch.cuda.synchronize(dev)  # the H2D runs on torch's stream, the solve on ctx's
+        gen = dist_admm.admm_rank(backend, g, slabs, rank, ip_, im_, cfg=cfg)
+        if dist is None:
+            r = dist_admm.run_lockstep([gen], dist_admm.torch_cat, dist_admm.torch_split)[0]
+        else:
+            r = dist_admm.run_torch(gen, dist, dev)
+        if host:
+            for o, key in zip(out_h, ("b", "z", "u")):
+                o.copy_(r[key], non_blocking=True)
+        return r
+
+    def timed(host, k):
+        tot, launches = 0.0, 0
+        for _ in range(k):
+            torch.cuda.synchronize(dev)
+            if dist is not None:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            ctx.reset_launch_count()
+            e0.record(stream)
+            solve(host)
+            torch.cuda.synchronize(dev)
+            e1.record(stream)
+            e1.synchronize()
+            launches += ctx.launch_count()
+            tot += e0.elapsed_time(e1) / 1e3
+        return tot, launches
+
+    for _ in range(a.warmup):
+        solve(False)
+    with ClockSampler(local) as clk:
+        t_dev, launches = timed(False, a.steps)
+    t_e2e, _ = timed(True, a.steps)
+    from paper_1607_00531_b200 import shard
+    t_dev = shard.max_over_ranks(t_dev, dist, dev)
+    t_e2e = shard.max_over_ranks(t_e2e, dist, dev)
+    units = g.faces * iters * a.steps
+    ctx.profile(True)
+    ctx.profile_reset()
+    solve(False)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    kernels = [{"kernel": k, "ms_per_launch": ms / n, "launches": n}
+               for k, (ms, n) in sorted(prof.items(), key=lambda kv: -kv[1][0])[:8] if n]
+    cpu = None
+    if rank == 0 and not a.no_cpu_baseline:
+        try:
+            kind, dt, cores = cpu_reference(d, 1, os.cpu_count() or 1)
+            cpu = {"value": g.faces / dt, "unit": UNIT, "cores": cores, "kind": kind,
+                   "sample": f"1 ADMM iteration of the full {a.config} volume"}
+        except Exception as e:
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
+                   "sample": str(e)[:120]}
+    if rank == 0:
+        h2d = (ip_h.numel() + im_h.numel()) * 8 * world
+        line = {"metric": metric_for(a.config), "value": units / t_dev, "unit": UNIT,
+                "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+                "ms_per_step": t_dev / a.steps * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"ADMM {a.config} {'x'.join(map(str, g.dims()))}, "
+                                       f"{iters} iterations, fp64, from b=0, k-slabs over "
+                                       f"{world} GPU(s)",
+                           "faces": g.faces, "iterations": iters, "parallelism": f"kslab{world}",
+                           "l2": "working set > L2 (126 MB)"},
+                "e2e": {"value": units / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": 3 * g.faces * 8},
+                "gpu_launches": launches, "clocks": clk.summary(),
+                "roofline": {"bound": "hbm", "kernel": "admm_bstep", "achieved": None,
+                             "peak": None, "unit": "GB/s", "frac": None, "traffic": None,
+                             "note": "see the C3 line for the b-step roofline; per-kernel times "
+                                     "of one solve on rank 0 below", "kernels": kernels},
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     a = parse()
     iters = a.iters or DEFAULT_ITERS.get(a.config, 50)
     if a.impl == "reference":
         return run_reference_arm(a, iters)
+    if a.config == "C5":
+        return run_slabs(a, iters)
 
     import torch
     rank, world, local, dist = dist_setup(a.gpus)

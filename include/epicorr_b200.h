@@ -288,6 +288,47 @@ int epc_residual(epc_context* ctx, const epc_grid* g, int mem, const double* ipl
 /* Library build identity (arch, mode) for logs. */
 const char* epc_build_info(void);
 
+/* ---- slab-distributed ADMM building blocks -------------
+ * One volume split into k-slabs over ranks: rank r owns layers
+ * [k0, k0 + mk) of `full` in the reference face layout. These are the local
+ * steps of one admm_solve iteration (admm.cpp:488-560); the caller performs
+ * the collectives between them (paper_1607_00531_b200/dist_admm.py: two
+ * all-to-all transposes for the axis-3 DCT, a one-layer halo of z, an
+ * all-gather of the scalars). All pointers are device pointers.
+ * Rank blocks: on the sender, the block for rank s holds s's i range
+ * (shard_range over n1) of the local layers in the order [kl][j][il];
+ * concatenated over senders they form the receiver's i-slab layout
+ * il + ni (j + m2 k). */
+/* b_update (admm.cpp:301-443) on the slab's columns. sums3 = {max kkt,
+ * sum r^2, sum (D1 b)^2}; ints4 = {lowest failing column in the global
+ * numbering j + m2 k (-1: none), failure code, sqp iters, qp iters}. */
+int epc_slab_bstep(epc_context* ctx, const epc_grid* full, int k0, int mk, const double* iplus,
+                   const double* iminus, const double* b, const double* z, const double* u,
+                   double rho, const epc_objective_params* params, const epc_admm_config* cfg,
+                   double* b_out, double* sums3, long long* ints4);
+/* z_update first half (operators.cpp:388-400): rho V (b + u), the axis-2
+ * DCT (transform_axis2, operators.cpp:347-366), packed into rank blocks. */
+int epc_slab_zforward(epc_context* ctx, const epc_grid* full, int k0, int mk, int world,
+                      const double* b, const double* u, double rho, double* blocks);
+/* on an i-slab of ni faces per row: the axis-3 DCT, the spectral divide and
+ * the inverse axis-3 DCT (operators.cpp:367-386, 400-412). */
+int epc_slab_zsolve3(epc_context* ctx, const epc_grid* full, int ni, const double* in,
+                     double alpha, double rho, double* out);
+/* z_update second half: unpack, inverse axis-2 DCT -> z_new, and
+ * dual_update_and_residuals (admm.cpp:453-476): u_new = u_old + b - z_new;
+ * sums6 = {|b-z|^2, |z_old-z|^2, |b|^2, |z|^2, |u_new|^2, u_new.(b-z)}. */
+int epc_slab_zbackward(epc_context* ctx, const epc_grid* full, int k0, int mk, int world,
+                       const double* blocks, const double* b, const double* u_old,
+                       const double* z_old, double rho, double* z_new, double* u_new,
+                       double* sums6);
+/* g_value parts (admm.cpp:275-285): sums2 = {sum (D2 z)^2, sum (D3 z)^2}
+ * over the slab, the D3 terms across the upper boundary from `halo` (the
+ * next rank's first face layer; NULL on the last rank). */
+int epc_slab_zdiff(epc_context* ctx, const epc_grid* full, int k0, int mk, const double* z,
+                   const double* halo, double* sums2);
+/* x *= factor (the u rescale after a rho change, admm.cpp:546-552). */
+int epc_slab_scale(epc_context* ctx, long long n, double* x, double factor);
+
 #ifdef __cplusplus
 }
 #endif

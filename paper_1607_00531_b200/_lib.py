@@ -25,6 +25,8 @@ EXPORTS = [
     "epc_augmented_lagrangian", "epc_rho_schedule", "epc_qp_active_set_batch", "epc_gn_solve",
     "epc_objective_gn", "epc_gn_hessian_build", "epc_gn_hessian_apply", "epc_precond_apply",
     "epc_pcg", "epc_residual", "epc_build_info", "epc_bstep_timing", "epc_bstep_counters",
+    "epc_slab_bstep", "epc_slab_zforward", "epc_slab_zsolve3", "epc_slab_zbackward",
+    "epc_slab_zdiff", "epc_slab_scale",
 ]
 
 
@@ -90,6 +92,13 @@ def _declare(L):
     L.epc_build_info.restype = C.c_char_p
     L.epc_bstep_timing.argtypes = [X, C.POINTER(C.c_longlong)]
     L.epc_bstep_counters.argtypes = [X, C.POINTER(C.c_longlong)]
+    D, LL, I = C.POINTER(C.c_double), C.POINTER(C.c_longlong), C.c_int
+    L.epc_slab_bstep.argtypes = [X, G, I, I, X, X, X, X, X, C.c_double, P, A, X, D, LL]
+    L.epc_slab_zforward.argtypes = [X, G, I, I, I, X, X, C.c_double, X]
+    L.epc_slab_zsolve3.argtypes = [X, G, I, X, C.c_double, C.c_double, X]
+    L.epc_slab_zbackward.argtypes = [X, G, I, I, I, X, X, X, X, C.c_double, X, X, D]
+    L.epc_slab_zdiff.argtypes = [X, G, I, I, X, X, D]
+    L.epc_slab_scale.argtypes = [X, C.c_longlong, X, C.c_double]
 
 
 def load(build_if_missing=True):

@@ -197,3 +197,9 @@ __global__ void k_axpy_point(const double* x, const double* d, double t, double*
 __global__ void k_neg_norm(const double* g, double* r, long long n, double* partials);
 __global__ void k_dot2(const double* a, const double* b, long long n, double* partials);
 __global__ void k_gn_copy(const double* src, double* dst, long long n);
+
+// ---- slab-distributed ADMM data movement (slab.cu) -----------------------------
+__global__ void k_slab_transpose(const double* in, double* out, int n1, int m2, int mk, int world,
+                                 int to_blocks);
+__global__ void k_zdiff_halo(const double* last, const double* halo, long long n, double ih3,
+                             double* partials);

@@ -77,7 +77,14 @@ class Context:
         dev = [_is_dev(a) for a in arrays if a is not None]
         if any(dev) and not all(dev):
             raise ValueError("mix of host and device arrays")
-        return abi.EPC_MEM_DEVICE if dev and dev[0] else abi.EPC_MEM_HOST
+        if dev and dev[0]:
+            # device inputs may still be in flight on torch's stream; the
+            # library runs on the context's stream
+            import torch
+            first = next(a for a in arrays if a is not None)
+            torch.cuda.current_stream(first.device).synchronize()
+            return abi.EPC_MEM_DEVICE
+        return abi.EPC_MEM_HOST
 
     @staticmethod
     def _ptr(a):
