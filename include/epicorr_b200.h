@@ -329,6 +329,41 @@ int epc_slab_zdiff(epc_context* ctx, const epc_grid* full, int k0, int mk, const
 /* x *= factor (the u rescale after a rho change, admm.cpp:546-552). */
 int epc_slab_scale(epc_context* ctx, long long n, double* x, double factor);
 
+/* ---- GN-PCG in k-slabs (GN row) -------------------------------
+ * Vectors are *extended*: the owned layers [k0, k0 + mk) plus one halo layer
+ * below (lo = 1 unless k0 = 0) and above (hi = 1 unless k0 + mk = m3), in the
+ * face (cell) layout of layers k0 - lo .. k0 + mk + hi - 1. Sums cover the
+ * owned layers; halos are the caller's (paper_1607_00531_b200/dist_gn.py). */
+/* objective_gn (objective.cpp:231-264) partials: out8 = {sum r^2,
+ * sum (D1 b)^2, sum phi, max |D1 b|, sum (D2 b)^2, sum (D3 b)^2, sum grad.dir,
+ * max |b|}; grad_ext (owned faces) when need_grad; keep_jac for _hessian. */
+int epc_gnslab_objective(epc_context* ctx, const epc_grid* full, int k0, int mk, int lo, int hi,
+                         const double* iplus_ext, const double* iminus_ext, const double* b_ext,
+                         const epc_objective_params* params, int need_grad, double* grad_ext,
+                         const double* dir_ext, int keep_jac, double* out8);
+/* GnHessian blocks at b (objective.cpp:266-300) and the block-Jacobi
+ * factor of the owned columns (gn_pcg.cpp:48-54); fail_col = lowest global
+ * column with a nonpositive pivot or -1. */
+int epc_gnslab_hessian(epc_context* ctx, const epc_grid* full, int k0, int mk, int lo, int hi,
+                       const double* iplus_ext, const double* iminus_ext, const double* b_ext,
+                       const epc_objective_params* params, int precond, long long* fail_col);
+/* q = H p (GnHessian::apply, objective.cpp:302-331); pq = owned sum p.q. */
+int epc_gnslab_hv(epc_context* ctx, const epc_grid* full, int k0, int mk, int lo, int hi,
+                  const epc_objective_params* params, const double* p_ext, double* q_ext,
+                  double* pq);
+/* pcg update on owned columns (gn_pcg.cpp:114-120): if do_axpy d += a p,
+ * r -= a q; z = M^{-1} r; rr_rz = {sum r.r, sum r.z}. */
+int epc_gnslab_update(epc_context* ctx, const epc_grid* full, int k0, int mk, int lo, int hi,
+                      const epc_objective_params* params, int precond, double a, int do_axpy,
+                      double* d_ext, double* r_ext, double* z_ext, const double* p_ext,
+                      const double* q_ext, double* rr_rz);
+/* y = x + t d; r = -g with gg = sum g.g; ab_bb = {sum a.b, sum b.b}. */
+int epc_gnslab_axpy(epc_context* ctx, long long n, const double* x, double t, const double* d,
+                    double* y);
+int epc_gnslab_negate(epc_context* ctx, long long n, const double* g, double* r, double* gg);
+int epc_gnslab_dot(epc_context* ctx, long long n, const double* a, const double* b,
+                   double* ab_bb);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,9 @@ EXPORTS = [
     "epc_objective_gn", "epc_gn_hessian_build", "epc_gn_hessian_apply", "epc_precond_apply",
     "epc_pcg", "epc_residual", "epc_build_info", "epc_bstep_timing", "epc_bstep_counters",
     "epc_slab_bstep", "epc_slab_zforward", "epc_slab_zsolve3", "epc_slab_zbackward",
-    "epc_slab_zdiff", "epc_slab_scale",
+    "epc_slab_zdiff", "epc_slab_scale", "epc_gnslab_objective", "epc_gnslab_hessian",
+    "epc_gnslab_hv", "epc_gnslab_update", "epc_gnslab_axpy", "epc_gnslab_negate",
+    "epc_gnslab_dot",
 ]
 
 
@@ -99,6 +101,13 @@ def _declare(L):
     L.epc_slab_zbackward.argtypes = [X, G, I, I, I, X, X, X, X, C.c_double, X, X, D]
     L.epc_slab_zdiff.argtypes = [X, G, I, I, X, X, D]
     L.epc_slab_scale.argtypes = [X, C.c_longlong, X, C.c_double]
+    L.epc_gnslab_objective.argtypes = [X, G, I, I, I, I, X, X, X, P, I, X, X, I, D]
+    L.epc_gnslab_hessian.argtypes = [X, G, I, I, I, I, X, X, X, P, I, LL]
+    L.epc_gnslab_hv.argtypes = [X, G, I, I, I, I, P, X, X, D]
+    L.epc_gnslab_update.argtypes = [X, G, I, I, I, I, P, I, C.c_double, I, X, X, X, X, X, D]
+    L.epc_gnslab_axpy.argtypes = [X, C.c_longlong, X, C.c_double, X, X]
+    L.epc_gnslab_negate.argtypes = [X, C.c_longlong, X, X, D]
+    L.epc_gnslab_dot.argtypes = [X, C.c_longlong, X, X, D]
 
 
 def load(build_if_missing=True):

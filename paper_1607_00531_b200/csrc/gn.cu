@@ -58,13 +58,14 @@ __global__ void __launch_bounds__(256) k_gn_cells(GnCellArgs A) {
             A.jlo[e] = jl;
             A.jhi[e] = jh;
         }
-        s_r += r * r;
+        const bool own = e >= A.sum_lo && e < A.sum_hi;
+        if (own) s_r += r * r;
         const double d1 = (b1 - b0) * ih;  // diff_x1 (operators.cpp:40-52)
-        s_d += d1 * d1;
+        if (own) s_d += d1 * d1;
         const double ad = fabs(d1);
-        mx = (mx < ad) ? ad : mx;
+        if (own) mx = (mx < ad) ? ad : mx;
         if (A.beta > 0.0) {
-            s_p += phi_v(d1);
+            if (own) s_p += phi_v(d1);
             if (A.dphi) A.dphi[e] = wpen * phi_d1(d1) * ih;  // penalty(), objective.cpp:217
             if (A.phi2) A.phi2[e] = phi_d2(d1);
         }
@@ -106,12 +107,13 @@ __global__ void __launch_bounds__(256) k_gn_faces(GnFaceArgs A) {
         const int j = (int)(c % m2), k = (int)(c / m2);
         const double* b = A.b;
         const double bf = b[f];
+        const bool own = f >= A.sum_lo && f < A.sum_hi;
         // diff_perp sums (g_value / smoother value)
-        if (j + 1 < m2) {
+        if (own && j + 1 < m2) {
             const double o = (b[f + n1] - bf) * A.ih2;
             s2 += o * o;
         }
-        if (m3 > 1 && k + 1 < m3) {
+        if (own && m3 > 1 && k + 1 < m3) {
             const double o = (b[f + layer] - bf) * A.ih3;
             s3 += o * o;
         }
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(256) k_gn_faces(GnFaceArgs A) {
                 g += 1.0 * pg;
             }
             A.grad[f] = g;
-            if (A.dir) sgd += g * A.dir[f];
+            if (A.dir && own) sgd += g * A.dir[f];
         }
     }
     const double t0 = block_sum(s2, sh);
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(256) k_gn_hv(GnHvArgs A) {
         }
         A.y[f] = y;
         if (A.mode != 2) A.p_new[f] = x;
-        s += x * y;
+        if (f >= A.sum_lo && f < A.sum_hi) s += x * y;
     }
     const double t = block_sum(s, sh);
     if (threadIdx.x == 0 && A.partials) A.partials[blockIdx.x] = t;

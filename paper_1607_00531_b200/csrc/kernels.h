@@ -2,6 +2,8 @@
 #pragma once
 
 #include "common.cuh"
+#include <climits>
+
 #include "model.cuh"
 
 // ---- ADMM b-step (bstep.cu) ---------------------------------------------
@@ -123,6 +125,7 @@ struct GnCellArgs {
     double o1, V, beta;
     double *r, *jlo, *jhi, *dphi, *phi2;  // outputs (cells), any may be null except as needed
     double* partials;                      // per block: {r^2, (D1b)^2, phi, max|D1b|}
+    long long sum_lo = 0, sum_hi = LLONG_MAX;  // cells entering the sums (k-slab halos excluded)
 };
 struct GnFaceArgs {
     const double *b, *r, *jlo, *jhi, *dphi, *dir;
@@ -131,6 +134,7 @@ struct GnFaceArgs {
     double V, alpha, beta, w1, w2, w3, ih2, ih3;
     double* grad;      // null: sums only
     double* partials;  // per block: {(D2b)^2, (D3b)^2, grad.dir}
+    long long sum_lo = 0, sum_hi = LLONG_MAX;  // faces entering the sums
 };
 struct GnHessArgs {
     const double *jlo, *jhi, *phi2;
@@ -147,6 +151,7 @@ struct GnHvArgs {
     int m1, n1, m2, m3;
     long long nface;
     double* partials;
+    long long sum_lo = 0, sum_hi = LLONG_MAX;  // faces entering p.q
 };
 struct GnUpdArgs {
     double *d, *r, *z;

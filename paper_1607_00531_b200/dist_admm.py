@@ -203,6 +203,18 @@ def run_lockstep(gens, cat, split):
                 answers.append(buf)
         elif kind == "halo_up":
             answers = [reqs[r + 1][1] if r + 1 < world else None for r in range(world)]
+        elif kind == "halo2":
+            # ("halo2", x_ext, o0, o1, layer, lo, hi): first owned layer -> the
+            # lower rank's upper halo, last owned layer -> the upper rank's
+            # lower halo (in place)
+            for r in range(world):
+                x, o0, o1, lay = reqs[r][1], reqs[r][2], reqs[r][3], reqs[r][4]
+                if r > 0:
+                    y, yo1 = reqs[r - 1][1], reqs[r - 1][3]
+                    y[yo1:yo1 + lay] = x[o0:o0 + lay]
+                if r + 1 < world:
+                    reqs[r + 1][1][0:lay] = x[o1 - lay:o1]
+            answers = [None] * world
         elif kind == "gather":
             vals = [list(r[1]) for r in reqs]
             answers = [vals] * world
@@ -251,6 +263,26 @@ def run_torch(gen, dist, device):
                     for w in dist.batch_isend_irecv(ops):
                         w.wait()
                 ans = None if got is None else _like(req[1], got)
+            elif kind == "halo2":
+                _, x, o0, o1, lay, lo, hi = req
+                tx = as_t(x)
+                ops = []
+                if lo:   # rank - 1 exists: its halo <- my first layer, mine <- its last
+                    ops.append(dist.P2POp(dist.isend, tx[o0:o0 + lay].contiguous(), rank - 1))
+                    lo_buf = torch.empty_like(tx[0:lay])
+                    ops.append(dist.P2POp(dist.irecv, lo_buf, rank - 1))
+                if hi:
+                    ops.append(dist.P2POp(dist.isend, tx[o1 - lay:o1].contiguous(), rank + 1))
+                    hi_buf = torch.empty_like(tx[0:lay])
+                    ops.append(dist.P2POp(dist.irecv, hi_buf, rank + 1))
+                if ops:
+                    for w in dist.batch_isend_irecv(ops):
+                        w.wait()
+                if lo:
+                    tx[0:lay].copy_(lo_buf)
+                if hi:
+                    tx[o1:o1 + lay].copy_(hi_buf)
+                ans = None
             elif kind == "gather":
                 t = torch.tensor(req[1], dtype=torch.float64, device=device)
                 outs = [torch.empty_like(t) for _ in range(world)]

@@ -130,3 +130,50 @@ def test_gloo_two_ranks_match_reference(oracle):
             rr.append(row)
         results.append(dict(b=b, z=z, u=u, rho=rho, stop=stop, rows=rr))
     _check_against_oracle(oracle, g, ip, im, results, dist_admm.Slabs(*M, world), cfg)
+
+
+# ---- the halo2 collective used by the GN slabs (dist_gn), gloo vs lockstep --
+HL = 3  # layer length
+
+
+def _halo_gen(rank, world, owned_layers=2):
+    lo = 1 if rank > 0 else 0
+    hi = 1 if rank + 1 < world else 0
+    n = (lo + owned_layers + hi) * HL
+    x = np.full(n, -1.0)
+    o0, o1 = lo * HL, (lo + owned_layers) * HL
+    x[o0:o1] = rank * 100 + np.arange(o1 - o0)
+    yield ("halo2", x, o0, o1, HL, lo, hi)
+    return x
+
+
+def _halo_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = dist_admm.run_torch(_halo_gen(rank, world), dist, torch.device("cpu"))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_halo2_gloo_matches_lockstep():
+    from dist_cpu_backend import np_cat, np_split
+    world = 3
+    want = dist_admm.run_lockstep([_halo_gen(r, world) for r in range(world)], np_cat, np_split)
+    # the lockstep exchange itself: halos hold the neighbours' edge layers
+    assert np.array_equal(want[0][-HL:], 100 + np.arange(HL))
+    assert np.array_equal(want[1][:HL], 3 + np.arange(HL))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert np.array_equal(got[r], want[r])
