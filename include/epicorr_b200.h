@@ -288,6 +288,43 @@ int epc_residual(epc_context* ctx, const epc_grid* g, int mem, const double* ipl
 /* Library build identity (arch, mode) for logs. */
 const char* epc_build_info(void);
 
+/* ---- multilevel (multilevel.hpp:13-63) -------------------- */
+enum { EPC_SOLVER_GN = 0, EPC_SOLVER_ADMM = 1 };
+/* AdmmRestart (multilevel.hpp:46-50) */
+enum { EPC_RESTART_PROLONG_ALL = 1, EPC_RESTART_B_FOR_BOTH = 2, EPC_RESTART_AVERAGE = 3 };
+/* SolveReport of a multilevel solve: both row lists appended level by level
+ * (report.cpp:23-28); stop / message are the last level's. */
+typedef struct {
+    int stop;
+    int n_admm_rows, n_gn_rows;
+    int b_level; /* the level whose grid b_out holds: nlev - 1, or the level an
+                    error / line-search failure stopped at (multilevel.cpp:246-249, 263) */
+    char message[256];
+} epc_multilevel_status;
+/* default_schedule (multilevel.cpp:22-41): coarse-to-fine grids into out[cap];
+ * host-only, no context. */
+int epc_default_schedule(const epc_grid* fine, int max_levels, int min_cells, epc_grid* out,
+                         int cap, int* nlev);
+/* restrict_image (multilevel.cpp:98-131): area-weighted block averaging of a
+ * cell field from `fine` to `coarse`. */
+int epc_restrict_image(epc_context* ctx, const epc_grid* fine, const epc_grid* coarse, int mem,
+                       const double* in, double* out);
+/* prolong_field (multilevel.cpp:157-203): linear interpolation of a face
+ * field from `coarse` to `fine`, rescaled to max|D1 b| = 0.95 if infeasible. */
+int epc_prolong_field(epc_context* ctx, const epc_grid* coarse, const epc_grid* fine, int mem,
+                      const double* in, double* out);
+/* multilevel_solve (multilevel.cpp:205-289) over `levels` (coarse -> fine,
+ * the last equal to `fine`); per-level overrides gn_max_outer /
+ * admm_max_iter (NULL or -1 entries: none). The images stay on the device
+ * between levels. b_out: the finest field. */
+int epc_multilevel_solve(epc_context* ctx, const epc_grid* fine, int mem, const double* iplus,
+                         const double* iminus, const epc_grid* levels, int nlev,
+                         const int* gn_max_outer, const int* admm_max_iter, int solver,
+                         const epc_objective_params* params, const epc_gn_config* gn_cfg,
+                         const epc_admm_config* admm_cfg, int restart, double* b_out,
+                         epc_admm_row* admm_rows, int max_admm_rows, epc_gn_row* gn_rows,
+                         int max_gn_rows, epc_multilevel_status* status);
+
 /* ---- slab-distributed ADMM building blocks -------------
  * One volume split into k-slabs over ranks: rank r owns layers
  * [k0, k0 + mk) of `full` in the reference face layout. These are the local

@@ -1804,3 +1804,421 @@ done:
     free(b); free(grad); free(dir); free(trial); free(bnew); free(keep_grad); free(zero);
     return ret;
 }
+
+/* ==========================================================================
+ * multilevel (proj/src/multilevel.cpp) — restatement for the checker
+ * ========================================================================== */
+
+static double extent_of(const epc_grid* g, int a) { return g->m[a] * g->h[a]; } /* grid.hpp:36 */
+
+/* default_schedule, multilevel.cpp:22-41 */
+int oracle_default_schedule(const epc_grid* fine, int max_levels, int min_cells, epc_grid* out,
+                            int cap, int* nlev, char* msg, size_t msglen) {
+    G gf;
+    int rc = grid_make(fine, &gf, msg, msglen);
+    if (rc) return rc;
+    epc_grid tmp[64];
+    int n = 0;
+    tmp[n++] = *fine;
+    epc_grid cur = *fine;
+    while (n < max_levels && n < 64) {
+        epc_grid next = cur;
+        int ok = 1;
+        for (int a = 0; a < fine->dim; ++a) {
+            next.m[a] = (cur.m[a] + 1) / 2;
+            if (next.m[a] < min_cells) ok = 0;
+            next.h[a] = extent_of(fine, a) / next.m[a];
+        }
+        if (!ok || (next.m[0] == cur.m[0] && next.m[1] == cur.m[1] && next.m[2] == cur.m[2])) break;
+        tmp[n++] = next;
+        cur = next;
+    }
+    if (n > cap) {
+        set_msg(msg, msglen, "default_schedule: output capacity too small");
+        return EPC_ERR_INVALID_ARGUMENT;
+    }
+    for (int l = 0; l < n; ++l) out[l] = tmp[n - 1 - l]; /* std::reverse: coarse -> fine */
+    *nlev = n;
+    return EPC_OK;
+}
+
+/* make_axis_weights, multilevel.cpp:53-77: coarse interval c covers fine
+ * intervals first[c] .. first[c] + cnt[c] - 1 with weights overlap / Hc */
+typedef struct {
+    int* first;
+    int* off; /* offsets into w, size mc + 1 */
+    double* w;
+} AxisW;
+
+static AxisW axis_weights(int mf, int mc, double L) {
+    AxisW aw;
+    aw.first = (int*)calloc((size_t)mc, sizeof(int));
+    aw.off = (int*)calloc((size_t)mc + 1, sizeof(int));
+    aw.w = (double*)calloc((size_t)(mf + 2 * mc + 4), sizeof(double));
+    const double hf = L / mf, hc = L / mc;
+    int nw = 0;
+    for (int c = 0; c < mc; ++c) {
+        aw.off[c] = nw;
+        const double lo = c * hc, hi = (c + 1) * hc;
+        int f0 = (int)floor(lo / hf + 1e-12);
+        if (f0 < 0) f0 = 0;
+        aw.first[c] = f0;
+        for (int f = f0; f < mf; ++f) {
+            const double flo = f * hf, fhi = (f + 1) * hf;
+            if (flo >= hi - 1e-12 * hc && f > f0) break;
+            const double ov = dmin(hi, fhi) - dmax(lo, flo);
+            if (ov <= 0.0) {
+                if (f == f0) {
+                    aw.first[c] = f + 1;
+                    continue;
+                }
+                break;
+            }
+            aw.w[nw++] = ov / hc;
+        }
+    }
+    aw.off[mc] = nw;
+    return aw;
+}
+
+static void axis_free(AxisW* a) {
+    free(a->first);
+    free(a->off);
+    free(a->w);
+}
+
+/* restrict_axis, multilevel.cpp:79-94 */
+static double* restrict_axis(const double* in, long long pre, int mf, long long post,
+                             const AxisW* aw, int mc) {
+    double* out = dalloc(pre * mc * post);
+    for (long long p = 0; p < post; ++p)
+        for (int c = 0; c < mc; ++c) {
+            double* o = out + pre * (c + (long long)mc * p);
+            for (int t = 0; t < aw->off[c + 1] - aw->off[c]; ++t) {
+                const int f = aw->first[c] + t;
+                const double wt = aw->w[aw->off[c] + t];
+                const double* s = in + pre * (f + (long long)mf * p);
+                for (long long i = 0; i < pre; ++i) o[i] += wt * s[i];
+            }
+        }
+    return out;
+}
+
+/* restrict_image, multilevel.cpp:98-131 */
+int oracle_restrict_image(const epc_grid* fine, const epc_grid* coarse, const double* in,
+                          double* out, char* msg, size_t msglen) {
+    G gf, gc;
+    int rc = grid_make(fine, &gf, msg, msglen);
+    if (rc) return rc;
+    rc = grid_make(coarse, &gc, msg, msglen);
+    if (rc) return rc;
+    if (coarse->dim != fine->dim) {
+        set_msg(msg, msglen, "restrict_image: dimension mismatch");
+        return EPC_ERR_INVALID_ARGUMENT;
+    }
+    for (int a = 0; a < 3; ++a) {
+        if (coarse->m[a] > fine->m[a]) {
+            set_msg(msg, msglen, "restrict_image: coarse grid larger than fine");
+            return EPC_ERR_INVALID_ARGUMENT;
+        }
+        const double ef = extent_of(fine, a);
+        if (fabs(extent_of(coarse, a) - ef) > 1e-9 * dmax(1.0, ef) ||
+            fabs(coarse->origin[a] - fine->origin[a]) > 1e-12 * dmax(1.0, ef)) {
+            set_msg(msg, msglen, "restrict_image: domains differ");
+            return EPC_ERR_INVALID_ARGUMENT;
+        }
+    }
+    const int fm1 = fine->m[0], fm2 = fine->m[1], fm3 = fine->m[2];
+    const int cm1 = coarse->m[0], cm2 = coarse->m[1], cm3 = coarse->m[2];
+    AxisW a1 = axis_weights(fm1, cm1, extent_of(fine, 0));
+    double* d1 = restrict_axis(in, 1, fm1, (long long)fm2 * fm3, &a1, cm1);
+    axis_free(&a1);
+    AxisW a2 = axis_weights(fm2, cm2, extent_of(fine, 1));
+    double* d2 = restrict_axis(d1, cm1, fm2, fm3, &a2, cm2);
+    axis_free(&a2);
+    free(d1);
+    if (fine->dim == 3 && fm3 != cm3) {
+        AxisW a3 = axis_weights(fm3, cm3, extent_of(fine, 2));
+        double* d3 = restrict_axis(d2, (long long)cm1 * cm2, fm3, 1, &a3, cm3);
+        axis_free(&a3);
+        free(d2);
+        d2 = d3;
+    }
+    memcpy(out, d2, sizeof(double) * (size_t)gc.ncell);
+    free(d2);
+    return EPC_OK;
+}
+
+/* make_taps, multilevel.cpp:141-155 */
+typedef struct {
+    int i0, i1;
+    double w1;
+} Tap;
+
+static Tap* make_taps(int count_f, double x0f, double stepf, int count_c, double x0c,
+                      double stepc) {
+    Tap* t = (Tap*)calloc((size_t)count_f, sizeof(Tap));
+    for (int i = 0; i < count_f; ++i) {
+        const double x = x0f + i * stepf;
+        const double u = (x - x0c) / stepc;
+        if (u <= 0.0) {
+            t[i].i0 = 0, t[i].i1 = 0, t[i].w1 = 0.0;
+        } else if (u >= count_c - 1) {
+            t[i].i0 = count_c - 1, t[i].i1 = count_c - 1, t[i].w1 = 0.0;
+        } else {
+            const int i0 = (int)floor(u);
+            t[i].i0 = i0;
+            t[i].i1 = i0 + 1 < count_c - 1 ? i0 + 1 : count_c - 1;
+            t[i].w1 = u - i0;
+        }
+    }
+    return t;
+}
+
+/* the infeasibility rescue shared by prolong_field and the average restart
+ * (multilevel.cpp:200-201, 275-276) */
+static void rescue(const G* g, double* b) {
+    const double dmx = d1_norm_inf(g, b);
+    if (dmx > 1.0 - 1e-10) {
+        const double s = 0.95 / dmx;
+        for (long long i = 0; i < g->nface; ++i) b[i] *= s;
+    }
+}
+
+/* prolong_field, multilevel.cpp:157-203 */
+int oracle_prolong_field(const epc_grid* coarse, const epc_grid* fine, const double* in,
+                         double* out, char* msg, size_t msglen) {
+    G gf, gc;
+    int rc = grid_make(fine, &gf, msg, msglen);
+    if (rc) return rc;
+    rc = grid_make(coarse, &gc, msg, msglen);
+    if (rc) return rc;
+    if (fine->dim != coarse->dim) {
+        set_msg(msg, msglen, "prolong_field: dimension mismatch");
+        return EPC_ERR_INVALID_ARGUMENT;
+    }
+    for (int a = 0; a < 3; ++a) {
+        if (fine->m[a] < coarse->m[a]) {
+            set_msg(msg, msglen, "prolong_field: fine grid smaller than coarse");
+            return EPC_ERR_INVALID_ARGUMENT;
+        }
+        const double ef = extent_of(fine, a);
+        if (fabs(extent_of(coarse, a) - ef) > 1e-9 * dmax(1.0, ef)) {
+            set_msg(msg, msglen, "prolong_field: domains differ");
+            return EPC_ERR_INVALID_ARGUMENT;
+        }
+    }
+    Tap* t1 = make_taps(gf.n1, fine->origin[0], fine->h[0], gc.n1, coarse->origin[0],
+                        coarse->h[0]);
+    Tap* t2 = make_taps(gf.m2, fine->origin[1] + 0.5 * fine->h[1], fine->h[1], gc.m2,
+                        coarse->origin[1] + 0.5 * coarse->h[1], coarse->h[1]);
+    Tap* t3;
+    if (fine->dim == 3) {
+        t3 = make_taps(gf.m3, fine->origin[2] + 0.5 * fine->h[2], fine->h[2], gc.m3,
+                       coarse->origin[2] + 0.5 * coarse->h[2], coarse->h[2]);
+    } else {
+        t3 = (Tap*)calloc(1, sizeof(Tap));
+    }
+    for (int k = 0; k < gf.m3; ++k)
+        for (int j = 0; j < gf.m2; ++j)
+            for (int i = 0; i <= gf.m1; ++i) {
+                const Tap a = t1[i], b = t2[j], c = t3[k];
+                double v = 0.0;
+                for (int ck = 0; ck < 2; ++ck) {
+                    const double wk = ck ? c.w1 : 1.0 - c.w1;
+                    if (wk == 0.0) continue;
+                    const int kk = ck ? c.i1 : c.i0;
+                    for (int cj = 0; cj < 2; ++cj) {
+                        const double wj = cj ? b.w1 : 1.0 - b.w1;
+                        if (wj == 0.0) continue;
+                        const int jj = cj ? b.i1 : b.i0;
+                        for (int ci = 0; ci < 2; ++ci) {
+                            const double wi = ci ? a.w1 : 1.0 - a.w1;
+                            if (wi == 0.0) continue;
+                            const int ii = ci ? a.i1 : a.i0;
+                            v += wk * wj * wi * in[ii + (long long)gc.n1 * (jj + (long long)gc.m2 * kk)];
+                        }
+                    }
+                }
+                out[i + (long long)gf.n1 * (j + (long long)gf.m2 * k)] = v;
+            }
+    free(t1);
+    free(t2);
+    free(t3);
+    rescue(&gf, out);
+    return EPC_OK;
+}
+
+static int grid_eq(const epc_grid* a, const epc_grid* b) {
+    if (a->dim != b->dim) return 0;
+    for (int x = 0; x < 3; ++x)
+        if (a->m[x] != b->m[x] || a->h[x] != b->h[x] || a->origin[x] != b->origin[x]) return 0;
+    return 1;
+}
+
+/* multilevel_solve, multilevel.cpp:205-289 */
+int oracle_multilevel_solve(const epc_grid* fine, const double* iplus, const double* iminus,
+                            const epc_grid* levels, int nlev, const int* gn_max_outer,
+                            const int* admm_max_iter, int solver,
+                            const epc_objective_params* P, const epc_gn_config* gcfg,
+                            const epc_admm_config* acfg, int restart, double* b_out,
+                            epc_admm_row* arows, int max_arows, epc_gn_row* grows,
+                            int max_grows, epc_multilevel_status* st) {
+    char* msg = st->message;
+    const size_t ml = sizeof st->message;
+    st->stop = EPC_STOP_CONVERGED;
+    st->n_admm_rows = st->n_gn_rows = 0;
+    st->b_level = nlev - 1;
+    msg[0] = 0;
+    /* LevelSchedule::validate, multilevel.cpp:11-20 */
+    if (nlev < 1) {
+        set_msg(msg, ml, "LevelSchedule: no levels");
+        return EPC_ERR_INVALID_ARGUMENT;
+    }
+    G tmpg;
+    for (int l = 0; l < nlev; ++l) {
+        int rc = grid_make(&levels[l], &tmpg, msg, ml);
+        if (rc) return rc;
+    }
+    for (int l = 1; l < nlev; ++l)
+        for (int a = 0; a < 3; ++a)
+            if (levels[l - 1].m[a] > levels[l].m[a]) {
+                set_msg(msg, ml, "LevelSchedule: levels must be ordered coarse to fine");
+                return EPC_ERR_INVALID_ARGUMENT;
+            }
+    if (!grid_eq(&levels[nlev - 1], fine)) {
+        set_msg(msg, ml, "multilevel_solve: finest level must match the data grid");
+        return EPC_ERR_INVALID_ARGUMENT;
+    }
+    G gfine;
+    grid_make(fine, &gfine, msg, ml);
+    double *b_start = NULL, *sb = NULL, *sz = NULL, *su = NULL;
+    double rho = 0.0;
+    int rc = EPC_OK;
+    for (int lvl = 0; lvl < nlev; ++lvl) {
+        const epc_grid* g = &levels[lvl];
+        G gl;
+        grid_make(g, &gl, msg, ml);
+        const int finest = lvl == nlev - 1;
+        double *ip = NULL, *im = NULL;
+        const double *lip = iplus, *lim = iminus;
+        if (!finest) {
+            ip = dalloc(gl.ncell);
+            im = dalloc(gl.ncell);
+            if ((rc = oracle_restrict_image(fine, g, iplus, ip, msg, ml)) ||
+                (rc = oracle_restrict_image(fine, g, iminus, im, msg, ml)))
+                goto done;
+            lip = ip;
+            lim = im;
+        }
+        double* b = dalloc(gl.nface);
+        if (solver == EPC_SOLVER_GN) {
+            epc_gn_config cfg = *gcfg;
+            if (gn_max_outer && gn_max_outer[lvl] >= 0) cfg.max_outer = gn_max_outer[lvl];
+            if (lvl == 0) {
+                free(b_start);
+                b_start = dalloc(gl.nface);
+            }
+            epc_gn_row* rows = (epc_gn_row*)calloc((size_t)cfg.max_outer + 1, sizeof(epc_gn_row));
+            epc_solve_status s;
+            rc = oracle_gn_solve(g, lip, lim, b_start, b, P, &cfg, lvl, rows, cfg.max_outer + 1, &s);
+            if (rc == EPC_OK) {
+                for (int r = 0; r < s.nrows && r <= cfg.max_outer; ++r) {
+                    if (st->n_gn_rows < max_grows) grows[st->n_gn_rows] = rows[r];
+                    st->n_gn_rows++;
+                }
+                st->stop = s.stop;
+                if (s.message[0]) set_msg(msg, ml, "%s", s.message);
+            } else {
+                set_msg(msg, ml, "%s", s.message);
+            }
+            free(rows);
+            if (rc) {
+                free(b);
+                goto level_done;
+            }
+            if (finest || s.stop == EPC_STOP_ERROR || s.stop == EPC_STOP_LINE_SEARCH_FAILURE) {
+                memcpy(b_out, b, sizeof(double) * (size_t)gl.nface);
+                st->b_level = lvl;
+            }
+            if (s.stop == EPC_STOP_ERROR || s.stop == EPC_STOP_LINE_SEARCH_FAILURE) {
+                free(b), free(ip), free(im);
+                goto early;
+            }
+            if (!finest) {
+                G gn;
+                grid_make(&levels[lvl + 1], &gn, msg, ml);
+                free(b_start);
+                b_start = dalloc(gn.nface);
+                rc = oracle_prolong_field(g, &levels[lvl + 1], b, b_start, msg, ml);
+            }
+            free(b);
+        } else {
+            epc_admm_config cfg = *acfg;
+            if (admm_max_iter && admm_max_iter[lvl] >= 0) cfg.max_iter = admm_max_iter[lvl];
+            if (lvl == 0) {
+                free(sb), free(sz), free(su);
+                sb = dalloc(gl.nface), sz = dalloc(gl.nface), su = dalloc(gl.nface);
+                rho = cfg.rho0;
+            }
+            double *z = dalloc(gl.nface), *u = dalloc(gl.nface);
+            epc_admm_row* rows = (epc_admm_row*)calloc((size_t)cfg.max_iter + 1, sizeof(epc_admm_row));
+            epc_solve_status s;
+            rc = oracle_admm_solve(g, lip, lim, sb, sz, su, b, z, u, &rho, P, &cfg, lvl, rows,
+                                   cfg.max_iter + 1, &s);
+            if (rc == EPC_OK) {
+                for (int r = 0; r < s.nrows && r <= cfg.max_iter; ++r) {
+                    if (st->n_admm_rows < max_arows) arows[st->n_admm_rows] = rows[r];
+                    st->n_admm_rows++;
+                }
+                st->stop = s.stop;
+                if (s.message[0]) set_msg(msg, ml, "%s", s.message);
+            } else {
+                set_msg(msg, ml, "%s", s.message);
+            }
+            free(rows);
+            if (rc == EPC_OK && (finest || s.stop == EPC_STOP_ERROR)) {
+                memcpy(b_out, b, sizeof(double) * (size_t)gl.nface);
+                st->b_level = lvl;
+            }
+            if (rc == EPC_OK && s.stop == EPC_STOP_ERROR) {
+                free(b), free(z), free(u), free(ip), free(im);
+                goto early;
+            }
+            if (rc == EPC_OK && !finest) {
+                const epc_grid* gf = &levels[lvl + 1];
+                G gn;
+                grid_make(gf, &gn, msg, ml);
+                double *nb = dalloc(gn.nface), *nz = dalloc(gn.nface), *nu = dalloc(gn.nface);
+                if (restart == EPC_RESTART_PROLONG_ALL) {
+                    rc = oracle_prolong_field(g, gf, b, nb, msg, ml);
+                    if (!rc) rc = oracle_prolong_field(g, gf, z, nz, msg, ml);
+                    if (!rc) rc = oracle_prolong_field(g, gf, u, nu, msg, ml);
+                } else if (restart == EPC_RESTART_B_FOR_BOTH) {
+                    rc = oracle_prolong_field(g, gf, b, nb, msg, ml);
+                    memcpy(nz, nb, sizeof(double) * (size_t)gn.nface);
+                } else {
+                    double* zf = dalloc(gn.nface);
+                    rc = oracle_prolong_field(g, gf, b, nb, msg, ml);
+                    if (!rc) rc = oracle_prolong_field(g, gf, z, zf, msg, ml);
+                    for (long long i = 0; i < gn.nface; ++i) nb[i] = 0.5 * (nb[i] + zf[i]);
+                    rescue(&gn, nb);
+                    memcpy(nz, nb, sizeof(double) * (size_t)gn.nface);
+                    free(zf);
+                }
+                free(sb), free(sz), free(su);
+                sb = nb, sz = nz, su = nu;
+            }
+            free(b), free(z), free(u);
+        }
+    level_done:
+        free(ip);
+        free(im);
+        if (rc) goto done;
+    }
+early:
+    rc = EPC_OK;
+done:
+    free(b_start), free(sb), free(sz), free(su);
+    return rc;
+}

@@ -93,6 +93,16 @@ class Checker:
         L.oracle_pcg.argtypes = [G, dptr, dptr, dptr, P, C.c_int, dptr, C.c_double, C.c_int, dptr,
                                  C.POINTER(PcgResult), C.c_char_p, C.c_size_t]
         L.oracle_residual.argtypes = [G, dptr, dptr, dptr, dptr]
+        GA = C.POINTER(Grid)
+        IP = C.POINTER(C.c_int)
+        L.oracle_default_schedule.argtypes = [G, C.c_int, C.c_int, GA, C.c_int, IP, C.c_char_p,
+                                              C.c_size_t]
+        L.oracle_restrict_image.argtypes = [G, G, dptr, dptr, C.c_char_p, C.c_size_t]
+        L.oracle_prolong_field.argtypes = [G, G, dptr, dptr, C.c_char_p, C.c_size_t]
+        L.oracle_multilevel_solve.argtypes = [G, dptr, dptr, GA, C.c_int, IP, IP, C.c_int, P, N, A,
+                                              C.c_int, dptr, C.POINTER(AdmmRow), C.c_int,
+                                              C.POINTER(GnRow), C.c_int,
+                                              C.POINTER(abi.MultilevelStatus)]
         L.oracle_rho_schedule.argtypes = [C.c_int] + [C.c_double] * 7
         L.oracle_rho_schedule.restype = C.c_double
         L.oracle_set_threads.argtypes = [C.c_int]
@@ -225,6 +235,62 @@ class Checker:
                                  eta, max_iters, _p(d), C.byref(res), msg, 256)
         return dict(rc=rc, d=d, iters=res.iters, relres=res.relres, relres_prec=res.relres_prec,
                     reached_tol=bool(res.reached_tol), message=msg.value.decode())
+
+    # ---- multilevel (multilevel.cpp) ------------------------------------------
+    def default_schedule(self, fine, max_levels=4, min_cells=16):
+        out = (Grid * 64)()
+        n = C.c_int(0)
+        msg = C.create_string_buffer(256)
+        rc = self.lib.oracle_default_schedule(C.byref(fine), max_levels, min_cells, out, 64,
+                                              C.byref(n), msg, 256)
+        if rc:
+            raise ValueError(msg.value.decode())
+        return [out[i] for i in range(n.value)]
+
+    def restrict_image(self, fine, coarse, img):
+        out = np.zeros(coarse.cells)
+        msg = C.create_string_buffer(256)
+        rc = self.lib.oracle_restrict_image(C.byref(fine), C.byref(coarse), _p(img), _p(out), msg,
+                                            256)
+        if rc:
+            raise ValueError(msg.value.decode())
+        return out
+
+    def prolong_field(self, coarse, fine, b):
+        out = np.zeros(fine.faces)
+        msg = C.create_string_buffer(256)
+        rc = self.lib.oracle_prolong_field(C.byref(coarse), C.byref(fine), _p(b), _p(out), msg, 256)
+        if rc:
+            raise ValueError(msg.value.decode())
+        return out
+
+    def multilevel_solve(self, fine, ip, im, levels, solver, params=None, gn_cfg=None,
+                         admm_cfg=None, restart=abi.RESTART_AVERAGE, gn_max_outer=None,
+                         admm_max_iter=None):
+        params = params or ObjectiveParams()
+        gn_cfg = gn_cfg or GnConfig()
+        admm_cfg = admm_cfg or AdmmConfig()
+        nlev = len(levels)
+        lv = (Grid * nlev)(*levels)
+        ov = lambda xs: None if xs is None else (C.c_int * nlev)(*[(-1 if x is None else x) for x in xs])  # noqa: E731
+        cap_a = sum((admm_max_iter[l] if admm_max_iter and admm_max_iter[l] is not None
+                     else admm_cfg.max_iter) for l in range(nlev)) + nlev
+        cap_g = sum((gn_max_outer[l] if gn_max_outer and gn_max_outer[l] is not None
+                     else gn_cfg.max_outer) + 1 for l in range(nlev))
+        arows, grows = (AdmmRow * cap_a)(), (GnRow * cap_g)()
+        b = np.zeros(fine.faces)
+        st = abi.MultilevelStatus()
+        rc = self.lib.oracle_multilevel_solve(C.byref(fine), _p(ip), _p(im), lv, nlev,
+                                              ov(gn_max_outer), ov(admm_max_iter), solver,
+                                              C.byref(params), C.byref(gn_cfg), C.byref(admm_cfg),
+                                              restart, _p(b), arows, cap_a, grows, cap_g,
+                                              C.byref(st))
+        if rc:
+            raise ValueError(st.message.decode())
+        nb = levels[st.b_level].faces
+        return dict(b=b[:nb], b_level=st.b_level, stop=st.stop, message=st.message.decode(),
+                    admm_rows=abi.rows_to_dicts(arows, min(st.n_admm_rows, cap_a)),
+                    gn_rows=abi.rows_to_dicts(grows, min(st.n_gn_rows, cap_g)))
 
     def residual(self, g, ip, im, b):
         r = np.zeros(g.cells)

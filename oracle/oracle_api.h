@@ -89,6 +89,21 @@ double oracle_rho_schedule(int schedule, double rho, double rho_min, double prim
 /* Thread count used by the reference harness (ignored by the C restatement). */
 void oracle_set_threads(int threads);
 
+/* multilevel (multilevel.cpp): see the epc_* counterparts in epicorr_b200.h */
+int oracle_default_schedule(const epc_grid* fine, int max_levels, int min_cells, epc_grid* out,
+                            int cap, int* nlev, char* msg, size_t msglen);
+int oracle_restrict_image(const epc_grid* fine, const epc_grid* coarse, const double* in,
+                          double* out, char* msg, size_t msglen);
+int oracle_prolong_field(const epc_grid* coarse, const epc_grid* fine, const double* in,
+                         double* out, char* msg, size_t msglen);
+int oracle_multilevel_solve(const epc_grid* fine, const double* iplus, const double* iminus,
+                            const epc_grid* levels, int nlev, const int* gn_max_outer,
+                            const int* admm_max_iter, int solver,
+                            const epc_objective_params* p, const epc_gn_config* gcfg,
+                            const epc_admm_config* acfg, int restart, double* b_out,
+                            epc_admm_row* arows, int max_arows, epc_gn_row* grows,
+                            int max_grows, epc_multilevel_status* st);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,7 @@
 #include "epicorr/gn_pcg.hpp"
 #include "epicorr/grid.hpp"
 #include "epicorr/image.hpp"
+#include "epicorr/multilevel.hpp"
 #include "epicorr/objective.hpp"
 #include "epicorr/operators.hpp"
 
@@ -369,6 +370,98 @@ double oracle_rho_schedule(int schedule, double rho, double rho_min, double prim
                            double dual_res, double tau_incr, double tau_decr, double mu) {
     return rho_schedule(RhoSchedule(schedule), rho, rho_min, primal_res, dual_res, tau_incr,
                         tau_decr, mu);
+}
+
+
+int oracle_default_schedule(const epc_grid* fine, int max_levels, int min_cells, epc_grid* out,
+                            int cap, int* nlev, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const LevelSchedule s = default_schedule(to_grid(fine), max_levels, min_cells);
+        if (s.levels() > cap) throw std::invalid_argument("default_schedule: output capacity too small");
+        for (int l = 0; l < s.levels(); ++l) {
+            out[l].dim = s.grids[l].dim;
+            for (int a = 0; a < 3; ++a) {
+                out[l].m[a] = s.grids[l].m[a];
+                out[l].h[a] = s.grids[l].h[a];
+                out[l].origin[a] = s.grids[l].origin[a];
+            }
+        }
+        *nlev = s.levels();
+    });
+}
+
+int oracle_restrict_image(const epc_grid* fine, const epc_grid* coarse, const double* in,
+                          double* out, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec gf = to_grid(fine);
+        const ImageVolume r = restrict_image(cells(gf, in), to_grid(coarse));
+        std::memcpy(out, r.v.data(), sizeof(double) * r.v.size());
+    });
+}
+
+int oracle_prolong_field(const epc_grid* coarse, const epc_grid* fine, const double* in,
+                         double* out, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec gc = to_grid(coarse);
+        copy_out(prolong_field(faces(gc, in), to_grid(fine)), out);
+    });
+}
+
+int oracle_multilevel_solve(const epc_grid* fine, const double* iplus, const double* iminus,
+                            const epc_grid* levels, int nlev, const int* gn_max_outer,
+                            const int* admm_max_iter, int solver,
+                            const epc_objective_params* p, const epc_gn_config* gcfg,
+                            const epc_admm_config* acfg, int restart, double* b_out,
+                            epc_admm_row* arows, int max_arows, epc_gn_row* grows,
+                            int max_grows, epc_multilevel_status* st) {
+    st->stop = EPC_STOP_CONVERGED;
+    st->n_admm_rows = st->n_gn_rows = 0;
+    st->b_level = nlev - 1;
+    return guarded(st->message, sizeof st->message, [&] {
+        const GridSpec g = to_grid(fine);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        LevelSchedule sched;
+        for (int l = 0; l < nlev; ++l) {
+            GridSpec s;
+            s.dim = levels[l].dim;
+            for (int a = 0; a < 3; ++a) {
+                s.m[a] = levels[l].m[a];
+                s.h[a] = levels[l].h[a];
+                s.origin[a] = levels[l].origin[a];
+            }
+            sched.grids.push_back(s);
+        }
+        if (gn_max_outer || admm_max_iter) {
+            sched.overrides.resize(nlev);
+            for (int l = 0; l < nlev; ++l) {
+                if (gn_max_outer && gn_max_outer[l] >= 0) sched.overrides[l].gn_max_outer = gn_max_outer[l];
+                if (admm_max_iter && admm_max_iter[l] >= 0) sched.overrides[l].admm_max_iter = admm_max_iter[l];
+            }
+        }
+        const MultilevelResult res = multilevel_solve(
+            pair, sched, solver == EPC_SOLVER_GN ? SolverKind::gn : SolverKind::admm, to_params(p),
+            to_gn(gcfg), to_admm(acfg), AdmmRestart(restart));
+        for (int l = 0; l < nlev; ++l)
+            if (res.b.grid == sched.grids[l]) st->b_level = l;
+        copy_out(res.b, b_out);
+        for (std::size_t i = 0; i < res.report.admm.size(); ++i) {
+            const AdmmIterRow& r = res.report.admm[i];
+            if (int(i) < max_arows)
+                arows[i] = epc_admm_row{r.level,   r.iter,       r.primal_res, r.dual_res,
+                                        r.eps_pri, r.eps_dual,   r.rho,        r.lagrangian,
+                                        r.kkt_violation, r.b_update_s, r.wall_s};
+        }
+        for (std::size_t i = 0; i < res.report.gn.size(); ++i) {
+            const GnIterRow& r = res.report.gn[i];
+            if (int(i) < max_grows)
+                grows[i] = epc_gn_row{r.level,     r.iter,       r.j_value,        r.grad_norm, r.step,
+                                      r.pcg_iters, r.pcg_relres, r.pcg_relres_prec, r.wall_s};
+        }
+        st->n_admm_rows = int(res.report.admm.size());
+        st->n_gn_rows = int(res.report.gn.size());
+        st->stop = int(res.report.stop);
+        std::snprintf(st->message, sizeof st->message, "%s", res.report.message.c_str());
+    });
 }
 
 } // extern "C"

@@ -7,6 +7,7 @@ import os
 import threading
 
 from .abi import (AdmmConfig, AdmmRow, BUpdateStats, DualResult, GnConfig, GnRow, Grid,
+                  MultilevelStatus,
                   ObjectiveEval, ObjectiveParams, PcgResult, SolveStatus, dptr, iptr)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -28,7 +29,8 @@ EXPORTS = [
     "epc_slab_bstep", "epc_slab_zforward", "epc_slab_zsolve3", "epc_slab_zbackward",
     "epc_slab_zdiff", "epc_slab_scale", "epc_gnslab_objective", "epc_gnslab_hessian",
     "epc_gnslab_hv", "epc_gnslab_update", "epc_gnslab_axpy", "epc_gnslab_negate",
-    "epc_gnslab_dot",
+    "epc_gnslab_dot", "epc_default_schedule", "epc_restrict_image", "epc_prolong_field",
+    "epc_multilevel_solve",
 ]
 
 
@@ -108,6 +110,14 @@ def _declare(L):
     L.epc_gnslab_axpy.argtypes = [X, C.c_longlong, X, C.c_double, X, X]
     L.epc_gnslab_negate.argtypes = [X, C.c_longlong, X, X, D]
     L.epc_gnslab_dot.argtypes = [X, C.c_longlong, X, X, D]
+    GA = C.POINTER(Grid)
+    IPT = C.POINTER(C.c_int)
+    L.epc_default_schedule.argtypes = [G, I, I, GA, I, IPT]
+    L.epc_restrict_image.argtypes = [X, G, G, I, X, X]
+    L.epc_prolong_field.argtypes = [X, G, G, I, X, X]
+    L.epc_multilevel_solve.argtypes = [X, G, I, X, X, GA, I, IPT, IPT, I, P, N, A, I, X,
+                                       C.POINTER(AdmmRow), I, C.POINTER(GnRow), I,
+                                       C.POINTER(MultilevelStatus)]
 
 
 def load(build_if_missing=True):

@@ -121,6 +121,17 @@ class GnRow(C.Structure):
                 ("wall_s", C.c_double)]
 
 
+SOLVER_GN, SOLVER_ADMM = 0, 1
+RESTART_PROLONG_ALL, RESTART_B_FOR_BOTH, RESTART_AVERAGE = 1, 2, 3
+
+
+class MultilevelStatus(C.Structure):
+    """epc_multilevel_status: SolveReport of a multilevel solve."""
+
+    _fields_ = [("stop", C.c_int), ("n_admm_rows", C.c_int), ("n_gn_rows", C.c_int),
+                ("b_level", C.c_int), ("message", C.c_char * 256)]
+
+
 class BUpdateStats(C.Structure):
     _fields_ = [("sqp_iters", C.c_long), ("qp_iters", C.c_long), ("kkt_violation", C.c_double),
                 ("max_active", C.c_int)]

@@ -98,6 +98,7 @@ enum Slot {
     S_GN0, S_GN1, S_GN2, S_GN3, S_GN4, S_GN5, S_GN6, S_GN7, S_GN8, S_GN9,
     S_X0, S_X1, S_X2, S_X3,
     S_SL0, S_SL1,
+    S_ML0, S_ML1, S_MLI, S_MLD, S_MLB, S_MLO, S_MLIP, S_MLIM, S_MLFIP, S_MLFIM,
     S_COUNT
 };
 
@@ -1198,4 +1199,5 @@ const char* epc_build_info(void) {
 
 #include "gn_host.inc"
 #include "slab_host.inc"
+#include "multilevel_host.inc"
 

@@ -208,3 +208,14 @@ __global__ void k_slab_transpose(const double* in, double* out, int n1, int m2, 
                                  int to_blocks);
 __global__ void k_zdiff_halo(const double* last, const double* halo, long long n, double ih3,
                              double* partials);
+
+// ---- multilevel (multilevel.cu) ------------------------------------------------
+struct MlTap {
+    int i0, i1;
+    double w1;  // value = (1 - w1) v[i0] + w1 v[i1]  (make_taps, multilevel.cpp:135-139)
+};
+__global__ void k_restrict_axis(const double* in, double* out, long long pre, int mf, int mc,
+                                long long post, const int* first, const int* off, const double* w);
+__global__ void k_prolong(const double* in, double* out, int fn1, int fm2, int fm3, int cn1,
+                          int cm2, const MlTap* t1, const MlTap* t2, const MlTap* t3);
+__global__ void k_average(double* b, const double* z, long long n);

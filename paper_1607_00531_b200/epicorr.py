@@ -289,6 +289,56 @@ class Context:
         return dict(b=bo, stop=st.stop, message=st.message.decode(),
                     rows=abi.rows_to_dicts(rows, min(st.nrows, cfg.max_outer + 1)))
 
+    # ---- multilevel (multilevel.hpp:13-63) -------------------------------------
+    def restrict_image(self, fine, coarse, img):
+        """restrict_image (multilevel.cpp:98-131)."""
+        mem = self._mem(img)
+        out = self._like(img, coarse.cells)
+        self._check(self.lib.epc_restrict_image(self.h, C.byref(fine), C.byref(coarse), mem,
+                                                self._ptr(img), self._ptr(out)))
+        return out
+
+    def prolong_field(self, coarse, fine, b):
+        """prolong_field (multilevel.cpp:157-203)."""
+        mem = self._mem(b)
+        out = self._like(b, fine.faces)
+        self._check(self.lib.epc_prolong_field(self.h, C.byref(coarse), C.byref(fine), mem,
+                                               self._ptr(b), self._ptr(out)))
+        return out
+
+    def multilevel_solve(self, fine, ip, im, levels, solver, params=None, gn_cfg=None,
+                         admm_cfg=None, restart=abi.RESTART_AVERAGE, gn_max_outer=None,
+                         admm_max_iter=None):
+        """multilevel_solve (multilevel.hpp:57-63). levels: coarse -> fine Grid
+        list (e.g. default_schedule(fine)); solver abi.SOLVER_GN / SOLVER_ADMM;
+        per-level overrides as lists (None entries: no override). Returns
+        dict(b, b_level, stop, message, admm_rows, gn_rows)."""
+        params = params or ObjectiveParams()
+        gn_cfg = gn_cfg or GnConfig()
+        admm_cfg = admm_cfg or AdmmConfig()
+        nlev = len(levels)
+        mem = self._mem(ip, im)
+        lv = (Grid * nlev)(*levels)
+        ov = lambda xs: None if xs is None else (C.c_int * nlev)(*[(-1 if x is None else x) for x in xs])  # noqa: E731
+        cap_a = sum((admm_max_iter[l] if admm_max_iter and admm_max_iter[l] is not None
+                     else admm_cfg.max_iter) for l in range(nlev)) + nlev
+        cap_g = sum((gn_max_outer[l] if gn_max_outer and gn_max_outer[l] is not None
+                     else gn_cfg.max_outer) + 1 for l in range(nlev))
+        arows, grows = (AdmmRow * cap_a)(), (GnRow * cap_g)()
+        b = self._like(ip, fine.faces)
+        st = abi.MultilevelStatus()
+        rc = self.lib.epc_multilevel_solve(self.h, C.byref(fine), mem, self._ptr(ip),
+                                           self._ptr(im), lv, nlev, ov(gn_max_outer),
+                                           ov(admm_max_iter), solver, C.byref(params),
+                                           C.byref(gn_cfg), C.byref(admm_cfg), restart,
+                                           self._ptr(b), arows, cap_a, grows, cap_g, C.byref(st))
+        if rc != 0:
+            _raise(rc, st.message.decode() or self._err())
+        nb = levels[st.b_level].faces
+        return dict(b=b[:nb], b_level=st.b_level, stop=st.stop, message=st.message.decode(),
+                    admm_rows=abi.rows_to_dicts(arows, min(st.n_admm_rows, cap_a)),
+                    gn_rows=abi.rows_to_dicts(grows, min(st.n_gn_rows, cap_g)))
+
     def objective_gn(self, g, ip, im, b, params=None, need_grad=True):
         params = params or ObjectiveParams()
         mem = self._mem(ip, im, b)
@@ -348,3 +398,14 @@ def context(device=0):
     if _default is None:
         _default = Context(device)
     return _default
+
+
+def default_schedule(fine, max_levels=4, min_cells=16):
+    """default_schedule (multilevel.cpp:22-41): coarse -> fine Grid list."""
+    L = load()
+    out = (Grid * 64)()
+    n = C.c_int(0)
+    rc = L.epc_default_schedule(C.byref(fine), max_levels, min_cells, out, 64, C.byref(n))
+    if rc != 0:
+        _raise(rc, "default_schedule: invalid grid")
+    return [out[i] for i in range(n.value)]
