@@ -32,6 +32,7 @@
 
 #include "epicorr/admm.hpp"
 #include "epicorr/gn_pcg.hpp"
+#include "epicorr/multilevel.hpp"
 #include "epicorr_b200.h"
 
 namespace {
@@ -254,6 +255,73 @@ GnSolveResult gauss_newton_solve(const VolumePair& pair, const StaggeredField& b
         const epc_gn_row& r = rows[i];
         out.report.gn.push_back(GnIterRow{r.level, r.iter, r.j_value, r.grad_norm, r.step,
                                           r.pcg_iters, r.pcg_relres, r.pcg_relres_prec, r.wall_s});
+    }
+    out.report.stop = StopReason(st.stop);
+    out.report.message = st.message;
+    return out;
+}
+
+
+// ---- multilevel (multilevel.hpp:37-63) on the device --------------------------
+ImageVolume restrict_image(const ImageVolume& img, const GridSpec& coarse) {
+    const epc_grid cf = to_c(img.grid), cc = to_c(coarse);
+    coarse.validate();
+    ImageVolume out(coarse);
+    check(epc_restrict_image(ctx(), &cf, &cc, EPC_MEM_HOST, img.v.data(), out.v.data()));
+    return out;
+}
+
+StaggeredField prolong_field(const StaggeredField& b_coarse, const GridSpec& fine) {
+    const epc_grid cc = to_c(b_coarse.grid), cf = to_c(fine);
+    fine.validate();
+    StaggeredField out(fine);
+    check(epc_prolong_field(ctx(), &cc, &cf, EPC_MEM_HOST, b_coarse.v.data(), out.v.data()));
+    return out;
+}
+
+MultilevelResult multilevel_solve(const VolumePair& pair, const LevelSchedule& schedule,
+                                  SolverKind solver, const ObjectiveParams& params,
+                                  const GNConfig& gn_config, const ADMMConfig& admm_config,
+                                  AdmmRestart restart) {
+    schedule.validate();
+    const int nlev = schedule.levels();
+    std::vector<epc_grid> lv;
+    for (const GridSpec& g : schedule.grids) lv.push_back(to_c(g));
+    std::vector<int> gmo, ami;
+    int cap_g = 0, cap_a = 0;
+    for (int l = 0; l < nlev; ++l) {
+        const bool has = !schedule.overrides.empty();
+        gmo.push_back(has && schedule.overrides[l].gn_max_outer ? *schedule.overrides[l].gn_max_outer : -1);
+        ami.push_back(has && schedule.overrides[l].admm_max_iter ? *schedule.overrides[l].admm_max_iter : -1);
+        cap_g += (gmo.back() >= 0 ? gmo.back() : gn_config.max_outer) + 1;
+        cap_a += (ami.back() >= 0 ? ami.back() : admm_config.max_iter) + 1;
+    }
+    const epc_grid cg = to_c(pair.grid());
+    const epc_objective_params cp = to_c(params);
+    const epc_gn_config gc = to_c(gn_config);
+    const epc_admm_config ac = to_c(admm_config);
+    std::vector<epc_admm_row> arows(cap_a);
+    std::vector<epc_gn_row> grows(cap_g);
+    std::vector<double> b(pair.grid().faces());
+    epc_multilevel_status st{};
+    const int rc = epc_multilevel_solve(
+        ctx(), &cg, EPC_MEM_HOST, pair.plus.v.data(), pair.minus.v.data(), lv.data(), nlev,
+        gmo.data(), ami.data(), solver == SolverKind::gn ? EPC_SOLVER_GN : EPC_SOLVER_ADMM, &cp,
+        &gc, &ac, int(restart), b.data(), arows.data(), cap_a, grows.data(), cap_g, &st);
+    if (rc != EPC_OK) rethrow(rc, st.message[0] ? st.message : epc_last_error(ctx()));
+    MultilevelResult out;
+    out.b = StaggeredField(schedule.grids[st.b_level]);
+    std::memcpy(out.b.v.data(), b.data(), sizeof(double) * out.b.v.size());
+    for (int i = 0; i < std::min(st.n_gn_rows, cap_g); ++i) {
+        const epc_gn_row& r = grows[i];
+        out.report.gn.push_back(GnIterRow{r.level, r.iter, r.j_value, r.grad_norm, r.step,
+                                          r.pcg_iters, r.pcg_relres, r.pcg_relres_prec, r.wall_s});
+    }
+    for (int i = 0; i < std::min(st.n_admm_rows, cap_a); ++i) {
+        const epc_admm_row& r = arows[i];
+        out.report.admm.push_back(AdmmIterRow{r.level, r.iter, r.primal_res, r.dual_res, r.eps_pri,
+                                              r.eps_dual, r.rho, r.lagrangian, r.kkt_violation,
+                                              r.b_update_s, r.wall_s});
     }
     out.report.stop = StopReason(st.stop);
     out.report.message = st.message;
