@@ -288,6 +288,21 @@ int epc_residual(epc_context* ctx, const epc_grid* g, int mem, const double* ipl
 /* Library build identity (arch, mode) for logs. */
 const char* epc_build_info(void);
 
+/* ---- either side of the solve (image.hpp:62-86) -------- */
+/* correct_pair (image.cpp:226-253): the two corrected volumes. */
+int epc_correct_pair(epc_context* ctx, const epc_grid* grid, int mem, const double* iplus,
+                     const double* iminus, const double* b, double* out_plus, double* out_minus);
+/* ssd (image.cpp:255-263) and ncc (:265-283) of two cell fields. */
+int epc_ssd(epc_context* ctx, const epc_grid* grid, int mem, const double* a, const double* b,
+            double* out);
+int epc_ncc(epc_context* ctx, const epc_grid* grid, int mem, const double* a, const double* b,
+            double* out);
+/* simulate_pair (image.cpp:187-224) with SimulateOptions {noise_sigma, seed,
+ * feas_margin} (image.hpp:62-66). */
+int epc_simulate_pair(epc_context* ctx, const epc_grid* grid, int mem, const double* truth,
+                      const double* b_true, double noise_sigma, unsigned long long seed,
+                      double feas_margin, double* out_plus, double* out_minus);
+
 /* ---- multilevel (multilevel.hpp:13-63) -------------------- */
 enum { EPC_SOLVER_GN = 0, EPC_SOLVER_ADMM = 1 };
 /* AdmmRestart (multilevel.hpp:46-50) */

@@ -2222,3 +2222,220 @@ done:
     free(b_start), free(sb), free(sz), free(su);
     return rc;
 }
+
+/* ==========================================================================
+ * image.cpp: correct_pair, ssd, ncc, simulate_pair — restatement
+ * ========================================================================== */
+
+/* correct_pair, image.cpp:226-253 */
+int oracle_correct_pair(const epc_grid* gg, const double* iplus, const double* iminus,
+                        const double* b, double* cp, double* cm, char* msg, size_t msglen) {
+    G g;
+    int rc = grid_make(gg, &g, msg, msglen);
+    if (rc) return rc;
+    if (d1_norm_inf(&g, b) > 1.0) {
+        set_msg(msg, msglen, "correct_pair: field infeasible, |D1 b| > 1");
+        return EPC_ERR_INVALID_ARGUMENT;
+    }
+    for (long long c = 0; c < g.ncol; ++c) {
+        const Interp ip = column_of(&g, iplus, c), im = column_of(&g, iminus, c);
+        const double* bc = b + c * g.n1;
+        for (int i = 0; i < g.m1; ++i) {
+            const double xc = g.o1 + (i + 0.5) * g.h1;
+            const double a = 0.5 * (bc[i] + bc[i + 1]);
+            const double d = (bc[i + 1] - bc[i]) / g.h1;
+            cp[c * g.m1 + i] = ip_value(&ip, xc + a) * (1.0 + d);
+            cm[c * g.m1 + i] = ip_value(&im, xc - a) * (1.0 - d);
+        }
+    }
+    return EPC_OK;
+}
+
+/* ssd, image.cpp:255-263 */
+int oracle_ssd(const epc_grid* gg, const double* a, const double* b, double* out, char* msg,
+               size_t msglen) {
+    G g;
+    int rc = grid_make(gg, &g, msg, msglen);
+    if (rc) return rc;
+    double s = 0.0;
+    for (long long i = 0; i < g.ncell; ++i) {
+        const double d = a[i] - b[i];
+        s += d * d;
+    }
+    *out = 0.5 * g.V * s;
+    return EPC_OK;
+}
+
+/* ncc, image.cpp:265-283 */
+int oracle_ncc(const epc_grid* gg, const double* a, const double* b, double* out, char* msg,
+               size_t msglen) {
+    G g;
+    int rc = grid_make(gg, &g, msg, msglen);
+    if (rc) return rc;
+    const long long n = g.ncell;
+    double ma = 0.0, mb = 0.0;
+    for (long long i = 0; i < n; ++i) {
+        ma += a[i];
+        mb += b[i];
+    }
+    ma /= (double)n;
+    mb /= (double)n;
+    double sab = 0.0, saa = 0.0, sbb = 0.0;
+    for (long long i = 0; i < n; ++i) {
+        const double da = a[i] - ma, db = b[i] - mb;
+        sab += da * db;
+        saa += da * da;
+        sbb += db * db;
+    }
+    if (saa <= 0.0 || sbb <= 0.0) {
+        set_msg(msg, msglen, "ncc: zero-variance image");
+        return EPC_ERR_INVALID_ARGUMENT;
+    }
+    *out = (sab * sab) / (saa * sbb);
+    return EPC_OK;
+}
+
+/* std::mt19937_64 (the standard's parameters) */
+typedef struct {
+    unsigned long long mt[312];
+    int i;
+} Mt64;
+
+static void mt64_seed(Mt64* s, unsigned long long seed) {
+    s->mt[0] = seed;
+    for (int i = 1; i < 312; ++i)
+        s->mt[i] = 6364136223846793005ULL * (s->mt[i - 1] ^ (s->mt[i - 1] >> 62)) + (unsigned long long)i;
+    s->i = 312;
+}
+
+static unsigned long long mt64_next(Mt64* s) {
+    if (s->i >= 312) {
+        for (int k = 0; k < 312; ++k) {
+            const unsigned long long y = (s->mt[k] & 0xFFFFFFFF80000000ULL) |
+                                         (s->mt[(k + 1) % 312] & 0x7FFFFFFFULL);
+            s->mt[k] = s->mt[(k + 156) % 312] ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+        }
+        s->i = 0;
+    }
+    unsigned long long x = s->mt[s->i++];
+    x ^= (x >> 29) & 0x5555555555555555ULL;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+    x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+    x ^= x >> 43;
+    return x;
+}
+
+/* std::generate_canonical<double, 53> over mt19937_64 (libstdc++): one draw */
+static double canonical(Mt64* s) {
+    const double sum = (double)mt64_next(s) * 1.0;
+    double r = sum / 18446744073709551616.0; /* 2^64 */
+    if (r >= 1.0) r = nextafter(1.0, 0.0);
+    return r;
+}
+
+/* std::normal_distribution<double> (libstdc++: Marsaglia polar, one cached value) */
+typedef struct {
+    double mean, stddev, saved;
+    int have;
+} Normal;
+
+static double normal_next(Normal* d, Mt64* s) {
+    double ret;
+    if (d->have) {
+        d->have = 0;
+        ret = d->saved;
+    } else {
+        double x, y, r2;
+        do {
+            x = 2.0 * canonical(s) - 1.0;
+            y = 2.0 * canonical(s) - 1.0;
+            r2 = x * x + y * y;
+        } while (r2 > 1.0 || r2 == 0.0);
+        const double mult = sqrt(-2 * log(r2) / r2);
+        d->saved = x * mult;
+        d->have = 1;
+        ret = y * mult;
+    }
+    return ret * d->stddev + d->mean;
+}
+
+/* FieldLine, image.cpp:143-162 */
+static double fl_value(const double* f, int n1, double h, double o, double x) {
+    const double u = (x - o) / h;
+    if (u <= 0.0) return f[0];
+    if (u >= n1 - 1) return f[n1 - 1];
+    const double fi = floor(u);
+    const int i = (int)fi;
+    const double w = u - fi;
+    return (1.0 - w) * f[i] + w * f[i + 1];
+}
+
+static double fl_slope(const double* f, int n1, double h, double o, double x) {
+    const double u = (x - o) / h;
+    if (u <= 0.0 || u >= n1 - 1) return 0.0;
+    double fi = floor(u);
+    if (fi == u) fi -= 1.0;
+    const int i = (int)fi < 0 ? 0 : (int)fi;
+    return (f[i + 1] - f[i]) / h;
+}
+
+/* invert_monotone, image.cpp:164-183 */
+static double invert_monotone(const double* f, int n1, double h, double o, double sign, double y,
+                              double tol) {
+    double bmax = 0.0;
+    for (int i = 0; i < n1; ++i) bmax = dmax(bmax, fabs(f[i]));
+    if (bmax == 0.0) return y;
+    double lo = y - bmax, hi = y + bmax;
+#define PSI(x) ((x) + sign * fl_value(f, n1, h, o, (x)) - y)
+    double flo = PSI(lo), fhi = PSI(hi);
+    while (flo > 0.0) {
+        lo -= bmax + h;
+        flo = PSI(lo);
+    }
+    while (fhi < 0.0) {
+        hi += bmax + h;
+        fhi = PSI(hi);
+    }
+    while (hi - lo > tol) {
+        const double mid = 0.5 * (lo + hi);
+        if (PSI(mid) <= 0.0) lo = mid;
+        else hi = mid;
+    }
+#undef PSI
+    return 0.5 * (lo + hi);
+}
+
+/* simulate_pair, image.cpp:187-224 */
+int oracle_simulate_pair(const epc_grid* gg, const double* truth, const double* b,
+                         double noise_sigma, unsigned long long seed, double feas_margin,
+                         double* up, double* um, char* msg, size_t msglen) {
+    G g;
+    int rc = grid_make(gg, &g, msg, msglen);
+    if (rc) return rc;
+    const double dmx = d1_norm_inf(&g, b);
+    if (dmx > 1.0 - feas_margin) {
+        set_msg(msg, msglen, "simulate_pair: field infeasible, max|D1 b| = %f", dmx);
+        return EPC_ERR_INVALID_ARGUMENT;
+    }
+    const double tol = 1e-10 * g.h1;
+    for (long long c = 0; c < g.ncol; ++c) {
+        const Interp tr = column_of(&g, truth, c);
+        const double* f = b + c * g.n1;
+        for (int i = 0; i < g.m1; ++i) {
+            const double y = g.o1 + (i + 0.5) * g.h1;
+            const double xp = invert_monotone(f, g.n1, g.h1, g.o1, +1.0, y, tol);
+            up[c * g.m1 + i] = ip_value(&tr, xp) / (1.0 + fl_slope(f, g.n1, g.h1, g.o1, xp));
+            const double xm = invert_monotone(f, g.n1, g.h1, g.o1, -1.0, y, tol);
+            um[c * g.m1 + i] = ip_value(&tr, xm) / (1.0 - fl_slope(f, g.n1, g.h1, g.o1, xm));
+        }
+    }
+    if (noise_sigma > 0.0) {
+        Mt64* s = (Mt64*)malloc(sizeof(Mt64));
+        mt64_seed(s, seed);
+        Normal d = {0.0, noise_sigma, 0.0, 0};
+        for (long long i = 0; i < g.ncell; ++i) up[i] += normal_next(&d, s);
+        for (long long i = 0; i < g.ncell; ++i) um[i] += normal_next(&d, s);
+        free(s);
+    }
+    return EPC_OK;
+}

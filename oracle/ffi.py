@@ -99,6 +99,11 @@ class Checker:
                                               C.c_size_t]
         L.oracle_restrict_image.argtypes = [G, G, dptr, dptr, C.c_char_p, C.c_size_t]
         L.oracle_prolong_field.argtypes = [G, G, dptr, dptr, C.c_char_p, C.c_size_t]
+        L.oracle_correct_pair.argtypes = [G, dptr, dptr, dptr, dptr, dptr, C.c_char_p, C.c_size_t]
+        L.oracle_ssd.argtypes = [G, dptr, dptr, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
+        L.oracle_ncc.argtypes = [G, dptr, dptr, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
+        L.oracle_simulate_pair.argtypes = [G, dptr, dptr, C.c_double, C.c_ulonglong, C.c_double,
+                                           dptr, dptr, C.c_char_p, C.c_size_t]
         L.oracle_multilevel_solve.argtypes = [G, dptr, dptr, GA, C.c_int, IP, IP, C.c_int, P, N, A,
                                               C.c_int, dptr, C.POINTER(AdmmRow), C.c_int,
                                               C.POINTER(GnRow), C.c_int,
@@ -235,6 +240,38 @@ class Checker:
                                  eta, max_iters, _p(d), C.byref(res), msg, 256)
         return dict(rc=rc, d=d, iters=res.iters, relres=res.relres, relres_prec=res.relres_prec,
                     reached_tol=bool(res.reached_tol), message=msg.value.decode())
+
+    # ---- image.cpp: correct_pair, ssd, ncc, simulate_pair -------------------------
+    def correct_pair(self, g, ip, im, b):
+        cp, cm = np.zeros(g.cells), np.zeros(g.cells)
+        msg = C.create_string_buffer(256)
+        rc = self.lib.oracle_correct_pair(C.byref(g), _p(ip), _p(im), _p(b), _p(cp), _p(cm), msg, 256)
+        if rc:
+            raise ValueError(msg.value.decode())
+        return cp, cm
+
+    def ssd(self, g, a, b):
+        out = C.c_double()
+        msg = C.create_string_buffer(256)
+        if self.lib.oracle_ssd(C.byref(g), _p(a), _p(b), C.byref(out), msg, 256):
+            raise ValueError(msg.value.decode())
+        return out.value
+
+    def ncc(self, g, a, b):
+        out = C.c_double()
+        msg = C.create_string_buffer(256)
+        if self.lib.oracle_ncc(C.byref(g), _p(a), _p(b), C.byref(out), msg, 256):
+            raise ValueError(msg.value.decode())
+        return out.value
+
+    def simulate_pair(self, g, truth, b_true, noise_sigma=0.0, seed=0, feas_margin=0.05):
+        up, um = np.zeros(g.cells), np.zeros(g.cells)
+        msg = C.create_string_buffer(256)
+        rc = self.lib.oracle_simulate_pair(C.byref(g), _p(truth), _p(b_true), noise_sigma, seed,
+                                           feas_margin, _p(up), _p(um), msg, 256)
+        if rc:
+            raise ValueError(msg.value.decode())
+        return up, um
 
     # ---- multilevel (multilevel.cpp) ------------------------------------------
     def default_schedule(self, fine, max_levels=4, min_cells=16):

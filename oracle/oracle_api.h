@@ -104,6 +104,18 @@ int oracle_multilevel_solve(const epc_grid* fine, const double* iplus, const dou
                             epc_admm_row* arows, int max_arows, epc_gn_row* grows,
                             int max_grows, epc_multilevel_status* st);
 
+/* image.cpp: correct_pair, ssd, ncc, simulate_pair */
+int oracle_correct_pair(const epc_grid* g, const double* iplus, const double* iminus,
+                        const double* b, double* out_plus, double* out_minus, char* msg,
+                        size_t msglen);
+int oracle_ssd(const epc_grid* g, const double* a, const double* b, double* out, char* msg,
+               size_t msglen);
+int oracle_ncc(const epc_grid* g, const double* a, const double* b, double* out, char* msg,
+               size_t msglen);
+int oracle_simulate_pair(const epc_grid* g, const double* truth, const double* b_true,
+                         double noise_sigma, unsigned long long seed, double feas_margin,
+                         double* out_plus, double* out_minus, char* msg, size_t msglen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -464,4 +464,48 @@ int oracle_multilevel_solve(const epc_grid* fine, const double* iplus, const dou
     });
 }
 
+
+int oracle_correct_pair(const epc_grid* gg, const double* iplus, const double* iminus,
+                        const double* b, double* out_plus, double* out_minus, char* msg,
+                        size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        auto [cp, cm] = correct_pair(pair, faces(g, b), g_threads);
+        std::memcpy(out_plus, cp.v.data(), sizeof(double) * cp.v.size());
+        std::memcpy(out_minus, cm.v.data(), sizeof(double) * cm.v.size());
+    });
+}
+
+int oracle_ssd(const epc_grid* gg, const double* a, const double* b, double* out, char* msg,
+               size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        *out = ssd(cells(g, a), cells(g, b));
+    });
+}
+
+int oracle_ncc(const epc_grid* gg, const double* a, const double* b, double* out, char* msg,
+               size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        *out = ncc(cells(g, a), cells(g, b));
+    });
+}
+
+int oracle_simulate_pair(const epc_grid* gg, const double* truth, const double* b_true,
+                         double noise_sigma, unsigned long long seed, double feas_margin,
+                         double* out_plus, double* out_minus, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        SimulateOptions o;
+        o.noise_sigma = noise_sigma;
+        o.seed = seed;
+        o.feas_margin = feas_margin;
+        const VolumePair p = simulate_pair(cells(g, truth), faces(g, b_true), o);
+        std::memcpy(out_plus, p.plus.v.data(), sizeof(double) * p.plus.v.size());
+        std::memcpy(out_minus, p.minus.v.data(), sizeof(double) * p.minus.v.size());
+    });
+}
+
 } // extern "C"

@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libepicorr_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["api.cu", "bstep.cu", "zstep.cu", "aux_kernels.cu", "gn.cu", "pcg.cu", "slab.cu", "multilevel.cu"]
+SOURCES = ["api.cu", "bstep.cu", "zstep.cu", "aux_kernels.cu", "gn.cu", "pcg.cu", "slab.cu", "multilevel.cu", "image.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-prec-div=true", "-prec-sqrt=true",
          "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-rdc=false", "--expt-relaxed-constexpr",

@@ -1200,4 +1200,5 @@ const char* epc_build_info(void) {
 #include "gn_host.inc"
 #include "slab_host.inc"
 #include "multilevel_host.inc"
+#include "image_host.inc"
 

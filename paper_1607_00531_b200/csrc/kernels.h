@@ -219,3 +219,14 @@ __global__ void k_restrict_axis(const double* in, double* out, long long pre, in
 __global__ void k_prolong(const double* in, double* out, int fn1, int fm2, int fm3, int cn1,
                           int cm2, const MlTap* t1, const MlTap* t2, const MlTap* t3);
 __global__ void k_average(double* b, const double* z, long long n);
+
+// ---- correct_pair / metrics / simulate_pair (image.cu) --------------------------
+void launch_correct_pair(epc_context* ctx, const double* ip, const double* im, const double* b,
+                         int m1, long long ncell, HDiv hd, double o1, double* cp, double* cm);
+__global__ void k_col_absmax(const double* b, int n1, long long ncol, double* out);
+void launch_simulate(epc_context* ctx, const double* truth, const double* b, const double* colmax,
+                     int m1, long long ncell, HDiv hd, double o1, double tol, double* up,
+                     double* um);
+__global__ void k_add(double* x, const double* n, long long len);
+__global__ void k_image_sums(const double* a, const double* b, long long n, int pass, double ma,
+                             double mb, double* partials);

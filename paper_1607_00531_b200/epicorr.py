@@ -289,6 +289,39 @@ class Context:
         return dict(b=bo, stop=st.stop, message=st.message.decode(),
                     rows=abi.rows_to_dicts(rows, min(st.nrows, cfg.max_outer + 1)))
 
+    # ---- either side of the solve (image.hpp:62-86) ------------------------------
+    def correct_pair(self, g, ip, im, b):
+        """correct_pair (image.cpp:226-253) -> (corrected plus, corrected minus)."""
+        mem = self._mem(ip, im, b)
+        cp, cm = self._like(ip, g.cells), self._like(ip, g.cells)
+        self._check(self.lib.epc_correct_pair(self.h, C.byref(g), mem, self._ptr(ip),
+                                              self._ptr(im), self._ptr(b), self._ptr(cp),
+                                              self._ptr(cm)))
+        return cp, cm
+
+    def ssd(self, g, a, b):
+        """ssd (image.cpp:255-263)."""
+        out = C.c_double()
+        self._check(self.lib.epc_ssd(self.h, C.byref(g), self._mem(a, b), self._ptr(a),
+                                     self._ptr(b), C.byref(out)))
+        return out.value
+
+    def ncc(self, g, a, b):
+        """ncc (image.cpp:265-283)."""
+        out = C.c_double()
+        self._check(self.lib.epc_ncc(self.h, C.byref(g), self._mem(a, b), self._ptr(a),
+                                     self._ptr(b), C.byref(out)))
+        return out.value
+
+    def simulate_pair(self, g, truth, b_true, noise_sigma=0.0, seed=0, feas_margin=0.05):
+        """simulate_pair (image.cpp:187-224) -> (I+, I-)."""
+        mem = self._mem(truth, b_true)
+        up, um = self._like(truth, g.cells), self._like(truth, g.cells)
+        self._check(self.lib.epc_simulate_pair(self.h, C.byref(g), mem, self._ptr(truth),
+                                               self._ptr(b_true), noise_sigma, seed, feas_margin,
+                                               self._ptr(up), self._ptr(um)))
+        return up, um
+
     # ---- multilevel (multilevel.hpp:13-63) -------------------------------------
     def restrict_image(self, fine, coarse, img):
         """restrict_image (multilevel.cpp:98-131)."""
