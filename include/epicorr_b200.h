@@ -303,6 +303,22 @@ int epc_simulate_pair(epc_context* ctx, const epc_grid* grid, int mem, const dou
                       const double* b_true, double noise_sigma, unsigned long long seed,
                       double feas_margin, double* out_plus, double* out_minus);
 
+/* ---- volume files and the phase-encoding permutation (volume_io.hpp) ------- */
+/* GridKind (volume_io.hpp:29) */
+enum { EPC_VOL_CELL = 0, EPC_VOL_FACE1 = 1, EPC_VOL_FACE2 = 2, EPC_VOL_FACE3 = 3 };
+/* write_volume / read_volume (volume_io.cpp:68-171): 512-byte EPIVOL 1 header,
+ * float32 little-endian payload. Host-only (no context). read: v = NULL
+ * returns the grid, kind and payload length n only. */
+int epc_write_volume(const char* path, const epc_grid* grid, int kind, const double* v);
+int epc_read_volume(const char* path, epc_grid* grid, int* kind, double* v, long long cap,
+                    long long* n);
+/* permute_to_axis1 (volume_io.cpp:203-209) of a cell volume, and
+ * unpermute_field (:211-223) of a face1 field, on the device. */
+int epc_permute_to_axis1(epc_context* ctx, const epc_grid* grid, int pe_axis, int mem,
+                         const double* in, double* out, epc_grid* out_grid);
+int epc_unpermute_field(epc_context* ctx, const epc_grid* grid, int pe_axis, int mem,
+                        const double* in, double* out, epc_grid* out_grid, int* kind);
+
 /* ---- multilevel (multilevel.hpp:13-63) -------------------- */
 enum { EPC_SOLVER_GN = 0, EPC_SOLVER_ADMM = 1 };
 /* AdmmRestart (multilevel.hpp:46-50) */

@@ -104,6 +104,13 @@ class Checker:
         L.oracle_ncc.argtypes = [G, dptr, dptr, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
         L.oracle_simulate_pair.argtypes = [G, dptr, dptr, C.c_double, C.c_ulonglong, C.c_double,
                                            dptr, dptr, C.c_char_p, C.c_size_t]
+        if hasattr(L, "oracle_write_volume"):  # reference harness only
+            L.oracle_write_volume.argtypes = [C.c_char_p, G, C.c_int, dptr, C.c_char_p, C.c_size_t]
+            L.oracle_read_volume.argtypes = [C.c_char_p, G, IP, dptr, C.c_longlong,
+                                             C.POINTER(C.c_longlong), C.c_char_p, C.c_size_t]
+            L.oracle_permute_to_axis1.argtypes = [G, C.c_int, dptr, dptr, G, C.c_char_p, C.c_size_t]
+            L.oracle_unpermute_field.argtypes = [G, C.c_int, dptr, dptr, G, IP, C.c_char_p,
+                                                 C.c_size_t]
         L.oracle_multilevel_solve.argtypes = [G, dptr, dptr, GA, C.c_int, IP, IP, C.c_int, P, N, A,
                                               C.c_int, dptr, C.POINTER(AdmmRow), C.c_int,
                                               C.POINTER(GnRow), C.c_int,
@@ -272,6 +279,38 @@ class Checker:
         if rc:
             raise ValueError(msg.value.decode())
         return up, um
+
+    # ---- volume_io (reference harness only) --------------------------------------
+    def write_volume(self, path, g, kind, v):
+        msg = C.create_string_buffer(256)
+        if self.lib.oracle_write_volume(path.encode(), C.byref(g), kind, _p(v), msg, 256):
+            raise RuntimeError(msg.value.decode())
+
+    def read_volume(self, path):
+        g, kind, n = Grid(), C.c_int(), C.c_longlong()
+        msg = C.create_string_buffer(256)
+        if self.lib.oracle_read_volume(path.encode(), C.byref(g), C.byref(kind), None, 0,
+                                       C.byref(n), msg, 256):
+            raise RuntimeError(msg.value.decode())
+        v = np.zeros(n.value)
+        self.lib.oracle_read_volume(path.encode(), C.byref(g), C.byref(kind), _p(v), n.value,
+                                    C.byref(n), msg, 256)
+        return g, kind.value, v
+
+    def permute_to_axis1(self, g, pe_axis, img):
+        out, og = np.zeros(g.cells), Grid()
+        msg = C.create_string_buffer(256)
+        if self.lib.oracle_permute_to_axis1(C.byref(g), pe_axis, _p(img), _p(out), C.byref(og), msg, 256):
+            raise ValueError(msg.value.decode())
+        return og, out
+
+    def unpermute_field(self, g, pe_axis, b):
+        out, og, kind = np.zeros(g.faces), Grid(), C.c_int()
+        msg = C.create_string_buffer(256)
+        if self.lib.oracle_unpermute_field(C.byref(g), pe_axis, _p(b), _p(out), C.byref(og),
+                                           C.byref(kind), msg, 256):
+            raise ValueError(msg.value.decode())
+        return og, kind.value, out
 
     # ---- multilevel (multilevel.cpp) ------------------------------------------
     def default_schedule(self, fine, max_levels=4, min_cells=16):

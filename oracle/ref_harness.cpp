@@ -18,6 +18,7 @@
 #include "epicorr/grid.hpp"
 #include "epicorr/image.hpp"
 #include "epicorr/multilevel.hpp"
+#include "epicorr/volume_io.hpp"
 #include "epicorr/objective.hpp"
 #include "epicorr/operators.hpp"
 
@@ -505,6 +506,63 @@ int oracle_simulate_pair(const epc_grid* gg, const double* truth, const double* 
         const VolumePair p = simulate_pair(cells(g, truth), faces(g, b_true), o);
         std::memcpy(out_plus, p.plus.v.data(), sizeof(double) * p.plus.v.size());
         std::memcpy(out_minus, p.minus.v.data(), sizeof(double) * p.minus.v.size());
+    });
+}
+
+
+// ---- volume_io (reference only; the product's counterparts are checked
+// against these in tests/test_volume_io.py) --------------------------------
+static epc_grid from_grid(const GridSpec& g) {
+    epc_grid o;
+    o.dim = g.dim;
+    for (int a = 0; a < 3; ++a) {
+        o.m[a] = g.m[a];
+        o.h[a] = g.h[a];
+        o.origin[a] = g.origin[a];
+    }
+    return o;
+}
+
+int oracle_write_volume(const char* path, const epc_grid* gg, int kind, const double* v,
+                        char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        VolumeData vd;
+        vd.grid = to_grid(gg);
+        vd.kind = GridKind(kind);
+        vd.v.assign(v, v + vd.payload_size());
+        write_volume(path, vd);
+    });
+}
+
+int oracle_read_volume(const char* path, epc_grid* g, int* kind, double* v, long long cap,
+                       long long* n, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const VolumeData vd = read_volume(path);
+        *g = from_grid(vd.grid);
+        *kind = int(vd.kind);
+        *n = (long long)vd.v.size();
+        if (v && cap >= *n) std::memcpy(v, vd.v.data(), sizeof(double) * vd.v.size());
+    });
+}
+
+int oracle_permute_to_axis1(const epc_grid* gg, int pe_axis, const double* in, double* out,
+                            epc_grid* out_grid, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        const ImageVolume r = permute_to_axis1(cells(g, in), pe_axis);
+        *out_grid = from_grid(r.grid);
+        std::memcpy(out, r.v.data(), sizeof(double) * r.v.size());
+    });
+}
+
+int oracle_unpermute_field(const epc_grid* gg, int pe_axis, const double* in, double* out,
+                           epc_grid* out_grid, int* kind, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumeData vd = unpermute_field(faces(g, in), pe_axis);
+        *out_grid = from_grid(vd.grid);
+        *kind = int(vd.kind);
+        std::memcpy(out, vd.v.data(), sizeof(double) * vd.v.size());
     });
 }
 

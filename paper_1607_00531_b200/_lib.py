@@ -30,7 +30,8 @@ EXPORTS = [
     "epc_slab_zdiff", "epc_slab_scale", "epc_gnslab_objective", "epc_gnslab_hessian",
     "epc_gnslab_hv", "epc_gnslab_update", "epc_gnslab_axpy", "epc_gnslab_negate",
     "epc_gnslab_dot", "epc_default_schedule", "epc_restrict_image", "epc_prolong_field",
-    "epc_multilevel_solve", "epc_correct_pair", "epc_ssd", "epc_ncc", "epc_simulate_pair",
+    "epc_multilevel_solve", "epc_correct_pair", "epc_ssd", "epc_ncc", "epc_simulate_pair", "epc_write_volume", "epc_read_volume",
+    "epc_permute_to_axis1", "epc_unpermute_field",
 ]
 
 
@@ -119,6 +120,10 @@ def _declare(L):
     L.epc_ssd.argtypes = [X, G, I, X, X, D]
     L.epc_ncc.argtypes = [X, G, I, X, X, D]
     L.epc_simulate_pair.argtypes = [X, G, I, X, X, C.c_double, C.c_ulonglong, C.c_double, X, X]
+    L.epc_write_volume.argtypes = [C.c_char_p, G, I, X]
+    L.epc_read_volume.argtypes = [C.c_char_p, G, IPT, X, C.c_longlong, LL]
+    L.epc_permute_to_axis1.argtypes = [X, G, I, I, X, X, G]
+    L.epc_unpermute_field.argtypes = [X, G, I, I, X, X, G, IPT]
     L.epc_multilevel_solve.argtypes = [X, G, I, X, X, GA, I, IPT, IPT, I, P, N, A, I, X,
                                        C.POINTER(AdmmRow), I, C.POINTER(GnRow), I,
                                        C.POINTER(MultilevelStatus)]

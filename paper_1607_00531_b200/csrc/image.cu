@@ -197,3 +197,26 @@ __global__ void __launch_bounds__(256) k_image_sums(const double* __restrict__ a
         o[3] = t3;
     }
 }
+
+// swap axes a and b of a 3D array (axis 0 fastest), dims d of the input
+// (swap_axes_raw, volume_io.cpp:184-201), thread per input element
+__global__ void k_swap_axes(const double* __restrict__ in, double* __restrict__ out, int d0, int d1,
+                            int d2, int a, int b) {
+    const long long n = (long long)d0 * d1 * d2;
+    int od[3] = {d0, d1, d2};
+    const int t = od[a];
+    od[a] = od[b];
+    od[b] = t;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
+        int idx[3];
+        idx[0] = (int)(e % d0);
+        const long long q = e / d0;
+        idx[1] = (int)(q % d1);
+        idx[2] = (int)(q / d1);
+        const int s = idx[a];
+        idx[a] = idx[b];
+        idx[b] = s;
+        out[idx[0] + (long long)od[0] * (idx[1] + (long long)od[1] * idx[2])] = in[e];
+    }
+}

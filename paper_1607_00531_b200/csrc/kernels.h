@@ -230,3 +230,4 @@ void launch_simulate(epc_context* ctx, const double* truth, const double* b, con
 __global__ void k_add(double* x, const double* n, long long len);
 __global__ void k_image_sums(const double* a, const double* b, long long n, int pass, double ma,
                              double mb, double* partials);
+__global__ void k_swap_axes(const double* in, double* out, int d0, int d1, int d2, int a, int b);

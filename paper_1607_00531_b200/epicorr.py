@@ -322,6 +322,22 @@ class Context:
                                                self._ptr(up), self._ptr(um)))
         return up, um
 
+    # ---- phase-encoding permutation (volume_io.hpp:45-53) -----------------------
+    def permute_to_axis1(self, g, pe_axis, img):
+        """permute_to_axis1 (volume_io.cpp:203-209) -> (grid, cells)."""
+        out, og = self._like(img, g.cells), Grid()
+        self._check(self.lib.epc_permute_to_axis1(self.h, C.byref(g), pe_axis, self._mem(img),
+                                                  self._ptr(img), self._ptr(out), C.byref(og)))
+        return og, out
+
+    def unpermute_field(self, g, pe_axis, b):
+        """unpermute_field (volume_io.cpp:211-223) -> (grid, kind, faces)."""
+        out, og, kind = self._like(b, g.faces), Grid(), C.c_int()
+        self._check(self.lib.epc_unpermute_field(self.h, C.byref(g), pe_axis, self._mem(b),
+                                                 self._ptr(b), self._ptr(out), C.byref(og),
+                                                 C.byref(kind)))
+        return og, kind.value, out
+
     # ---- multilevel (multilevel.hpp:13-63) -------------------------------------
     def restrict_image(self, fine, coarse, img):
         """restrict_image (multilevel.cpp:98-131)."""
@@ -442,3 +458,26 @@ def default_schedule(fine, max_levels=4, min_cells=16):
     if rc != 0:
         _raise(rc, "default_schedule: invalid grid")
     return [out[i] for i in range(n.value)]
+
+
+def write_volume(path, g, kind, v):
+    """write_volume (volume_io.cpp:68-100): EPIVOL 1, float32 payload."""
+    rc = load().epc_write_volume(str(path).encode(), C.byref(g), kind,
+                                 C.c_void_p(np.ascontiguousarray(v, dtype=np.float64).ctypes.data))
+    if rc != 0:
+        _raise(rc, f"write_volume: cannot write {path}")
+
+
+def read_volume(path):
+    """read_volume (volume_io.cpp:102-171) -> (grid, kind, values)."""
+    L = load()
+    g, kind, n = Grid(), C.c_int(), C.c_longlong()
+    rc = L.epc_read_volume(str(path).encode(), C.byref(g), C.byref(kind), None, 0, C.byref(n))
+    if rc != 0:
+        _raise(rc, f"read_volume: cannot read {path}")
+    v = np.zeros(n.value)
+    rc = L.epc_read_volume(str(path).encode(), C.byref(g), C.byref(kind),
+                           C.c_void_p(v.ctypes.data), n.value, C.byref(n))
+    if rc != 0:
+        _raise(rc, f"read_volume: cannot read {path}")
+    return g, kind.value, v
