@@ -165,8 +165,9 @@ int epc_bstep_timing(epc_context* ctx, long long* out10);
  * trials an enclosure could not decide, undecided stopping tests, failed
  * line searches, SQP iterations reaching the line search, exact fval
  * fallbacks, then a histogram of the accepted trial index (0, 1, 2-3, 4-7,
- * 8-15, 16-31, 32-39) and the failed-search count. */
-int epc_bstep_counters(epc_context* ctx, long long* out14);
+ * 8-15, 16-31, 32-39), the failed-search count, and the Schur solves
+ * (count, sum na, sum na^2, sum na^3). */
+int epc_bstep_counters(epc_context* ctx, long long* out18);
 /* Per-kernel CUDA-event timing on the context stream (for the roofline). */
 int epc_profile_enable(epc_context* ctx, int on);
 /* Fills up to `cap` entries: name (static string), total ms, launch count. */

@@ -412,7 +412,7 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
     P.qcap = qcap;
     P.counter = cnt;
     P.total_cols = total;
-    P.timing = (ctx->mode & EPC_MODE_BSTEP_TIMING) ? slot_t<long long>(ctx, S_GN9, 24) : nullptr;
+    P.timing = (ctx->mode & EPC_MODE_BSTEP_TIMING) ? slot_t<long long>(ctx, S_GN9, 28) : nullptr;
     P.cert = (ctx->mode & EPC_MODE_BSTEP_CHAINED) ? 0 : 1;
     EPC_LAUNCH(ctx, "admm_bstep", kern, (unsigned)slots, 32, smem, P);
     check_launch();
@@ -878,8 +878,8 @@ const char* epc_last_error(const epc_context* ctx) { return ctx ? ctx->last_erro
 int epc_set_mode(epc_context* ctx, int mode_bits) {
     return guarded(ctx, [&] {
         if ((mode_bits & EPC_MODE_BSTEP_TIMING) && !(ctx->mode & EPC_MODE_BSTEP_TIMING)) {
-            long long* t = slot_t<long long>(ctx, S_GN9, 24);
-            CK(cudaMemsetAsync(t, 0, 24 * sizeof(long long), ctx->stream));
+            long long* t = slot_t<long long>(ctx, S_GN9, 28);
+            CK(cudaMemsetAsync(t, 0, 28 * sizeof(long long), ctx->stream));
         }
         ctx->mode = mode_bits;
     });
@@ -887,16 +887,16 @@ int epc_set_mode(epc_context* ctx, int mode_bits) {
 
 int epc_bstep_timing(epc_context* ctx, long long* out10) {
     return guarded(ctx, [&] {
-        long long* t = slot_t<long long>(ctx, S_GN9, 24);
+        long long* t = slot_t<long long>(ctx, S_GN9, 28);
         d2h(ctx, out10, t, 10 * sizeof(long long));
         sync(ctx);
     });
 }
 
-int epc_bstep_counters(epc_context* ctx, long long* out14) {
+int epc_bstep_counters(epc_context* ctx, long long* out18) {
     return guarded(ctx, [&] {
-        long long* t = slot_t<long long>(ctx, S_GN9, 24);
-        d2h(ctx, out14, t + 10, 14 * sizeof(long long));
+        long long* t = slot_t<long long>(ctx, S_GN9, 28);
+        d2h(ctx, out18, t + 10, 18 * sizeof(long long));
         sync(ctx);
     });
 }

@@ -131,12 +131,12 @@ class Context:
 
     BSTEP_COUNTERS = ["ls_trials", "ls_undecided", "stop_undecided", "ls_failed", "ls_searches",
                       "fval_exact", "acc0", "acc1", "acc2_3", "acc4_7", "acc8_15", "acc16_31",
-                      "acc32_39", "fail"]
+                      "acc32_39", "fail", "schur_n", "schur_na", "schur_na2", "schur_na3"]
     MODE_BSTEP_TIMING = 1
     MODE_BSTEP_CHAINED = 1 << 13
 
     def bstep_counters(self):
-        out = (C.c_longlong * 14)()
+        out = (C.c_longlong * 18)()
         self._check(self.lib.epc_bstep_counters(self.h, out))
         return dict(zip(self.BSTEP_COUNTERS, list(out)))
 
