@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0, help="intensity scale (x400 variant)")
     ap.add_argument("--ref-iters", type=int, default=2, help="ADMM iterations per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gn", action="store_true", help="skip the GN-PCG leg (configs[1])")
+    ap.add_argument("--gn-config", default="C2")
     return ap.parse_args()
 
 
@@ -171,8 +173,147 @@ def run_reference_arm(a, iters):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": f"{a.ref_iters} ADMM iterations of the {a.config} solve per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not a.no_gn:
+        dg = synth.make_config(a.gn_config)
+        vals = []
+        for s_ in range(a.warmup + a.steps):
+            kind, dt, cores, npcg = gn_reference_sample(dg, threads)
+            if s_ >= a.warmup:
+                vals.append(dg.grid.faces * npcg / dt)
+        v = float(np.mean(vals))
+        line["gn"] = {"metric": f"voxel-iterations/s (GN-PCG, {'x'.join(map(str, dg.grid.dims()))}, fp64)",
+                      "value": v, "unit": GN_UNIT,
+                      "cpu_baseline": {"value": v, "unit": GN_UNIT, "cores": cores, "kind": kind,
+                                       "sample": f"1 GN step (<=50 PCG iterations) of the {a.gn_config} solve per step"},
+                      "e2e": {"value": v, "unit": GN_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+GN_UNIT = "face-PCG-iterations/s"
+
+
+def gn_config():
+    """BASELINE configs[1]: block-Jacobi GN-PCG, 10 GN steps x up to 50 PCG
+    iterations at eta = 1e-2; the outer stopping tests are disabled
+    (eps = 1e-300) so every run does exactly 10 GN steps."""
+    return abi.GnConfig(eta=1e-2, max_outer=10, max_pcg=50, eps_obj=1e-300, eps_iter=1e-300,
+                        eps_grad=1e-300, precond=abi.PRECOND_BLOCK_JACOBI)
+
+
+def gn_reference_sample(d, threads, outer=1):
+    """The reference's GN (oracle/_ref, else the C port) for `outer` GN steps
+    of the configs[1] solve -> (kind, seconds, cores, PCG iterations)."""
+    from oracle import ffi
+    kind = "reference" if os.path.exists(ffi.PATHS["ref"]) else "port"
+    chk = ffi.load("ref" if kind == "reference" else "oracle")
+    cfg = gn_config()
+    cfg.max_outer = outer
+    if kind == "reference":
+        chk.set_threads(threads)
+        cfg.threads = threads
+    t = time.perf_counter()
+    r = chk.gn_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
+    dt = time.perf_counter() - t
+    npcg = sum(x["pcg_iters"] for x in r["rows"])
+    return kind, dt, (threads if kind == "reference" else 1), npcg
+
+
+def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
+    """GN-PCG on configs[1] (C2 128x128x64): device-resident time to solution
+    and face-PCG-iterations/s, e2e through the C ABI with host buffers, the
+    PCG kernels against the HBM roof, and the reference CPU sample beside it."""
+    import ctypes as C
+
+    import torch
+    from dataclasses import replace
+    spec = synth.CONFIGS[a.gn_config]
+    spec = replace(spec, seed=spec.seed + 1000 * rank)
+    d = synth.make_pair(spec)
+    g = d.grid
+    cfg = gn_config()
+    ip_d, im_d = torch.from_numpy(d.iplus).to(dev), torch.from_numpy(d.iminus).to(dev)
+    ip_h, im_h = torch.from_numpy(d.iplus).pin_memory(), torch.from_numpy(d.iminus).pin_memory()
+    b0_h = torch.zeros(g.faces, dtype=torch.float64).pin_memory()
+    bo_h = torch.empty(g.faces, dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize(dev)
+
+    def solve_device():
+        return ctx.gn_solve(g, ip_d, im_d, cfg=cfg)
+
+    def solve_host():
+        rows = (abi.GnRow * (cfg.max_outer + 1))()
+        st = abi.SolveStatus()
+        P = lambda t: C.c_void_p(t.data_ptr())
+        rc = ctx.lib.epc_gn_solve(ctx.h, C.byref(g), abi.EPC_MEM_HOST, P(ip_h), P(im_h), P(b0_h),
+                                  P(bo_h), C.byref(abi.ObjectiveParams()), C.byref(cfg), 0, rows,
+                                  cfg.max_outer + 1, C.byref(st))
+        assert rc == 0, ctx._err()
+        return sum(rows[i].pcg_iters for i in range(min(st.nrows, cfg.max_outer + 1)))
+
+    def timed(fn, k):
+        tot, launches, npcg = 0.0, 0, 0
+        for _ in range(k):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ctx.reset_launch_count()
+            e0.record(stream)
+            r = fn()
+            e1.record(stream)
+            e1.synchronize()
+            launches += ctx.launch_count()
+            tot += e0.elapsed_time(e1) / 1e3
+            npcg += r if isinstance(r, int) else sum(x["pcg_iters"] for x in r["rows"])
+        return tot, launches, npcg
+
+    for _ in range(a.warmup):
+        solve_device()
+    t_dev, launches, npcg = timed(solve_device, a.steps)
+    t_e2e, _, npcg_h = timed(solve_host, a.steps)
+    from paper_1607_00531_b200 import shard
+    t_dev = shard.max_over_ranks(t_dev, dist, dev)
+    t_e2e = shard.max_over_ranks(t_e2e, dist, dev)
+    world = dist.get_world_size() if dist is not None else 1
+    # per-kernel times of one profiled solve; algorithmic bytes per face per
+    # launch (SURVEY 8(d)): pcg_hvp reads z, p_old, diag, off and writes p, q
+    # (48 B); pcg_update reads d, r, p, q, fd, fl and writes d, r, z (72 B)
+    ctx.profile(True)
+    ctx.profile_reset()
+    solve_device()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    per_face = {"pcg_update": 72, "pcg_hvp": 48}
+    kernels = []
+    for name, (ms, n) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
+        if not n:
+            continue
+        k = {"kernel": name, "launches": n, "ms_per_launch": ms / n,
+             "share": ms / sum(v[0] for v in prof.values())}
+        if name in per_face:
+            gbs = per_face[name] * g.faces / (ms / n / 1e3) / 1e9
+            k.update(alg_bytes=per_face[name] * g.faces, achieved_gbs=gbs)
+        kernels.append(k)
+    out = {"metric": f"voxel-iterations/s (GN-PCG, {'x'.join(map(str, g.dims()))}, fp64)",
+           "value": g.faces * npcg / t_dev * world, "unit": GN_UNIT,
+           "time_to_solution_s": t_dev / a.steps, "pcg_iterations_per_solve": npcg // a.steps,
+           "workload": f"GN-PCG {a.gn_config} block-Jacobi, 10 GN steps x <=50 PCG, eta 1e-2",
+           "e2e": {"value": g.faces * npcg_h / t_e2e * world, "unit": GN_UNIT,
+                   "h2d_bytes_per_step": (2 * g.cells + g.faces) * 8,
+                   "d2h_bytes_per_step": g.faces * 8},
+           "gpu_launches": launches, "kernels": kernels[:8],
+           "l2": "256 MB flush write before every timed step; the C2 PCG vectors (~85 MB) "
+                 "fit in L2 within a solve"}
+    if rank == 0 and not a.no_cpu_baseline:
+        try:
+            kind, dt, cores, np_ = gn_reference_sample(d, os.cpu_count() or 1)
+            out["cpu_baseline"] = {"value": g.faces * np_ / dt, "unit": GN_UNIT, "cores": cores,
+                                   "kind": kind, "sample": "1 GN step (<=50 PCG iterations) "
+                                                           f"of the {a.gn_config} solve"}
+        except Exception as e:
+            out["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(e)[:120]}
+    return out
 
 
 def run_slabs(a, iters):
@@ -467,6 +608,10 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
                    "sample": str(e)[:120]}
 
+    gn = None
+    if not a.no_gn and a.config != "C4":
+        gn = run_gn_leg(a, ctx, dev, stream, flush, rank, dist)
+
     if rank == 0:
         line = {"metric": metric_for(a.config), "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_max / a.steps * 1e3,
@@ -484,6 +629,8 @@ def main():
                         "d2h_bytes_per_step": 3 * nf * 8 * npairs},
                 "gpu_launches": launches, "clocks": clk.summary(),
                 "roofline": roofline, "cpu_baseline": cpu}
+        if gn is not None:
+            line["gn"] = gn
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

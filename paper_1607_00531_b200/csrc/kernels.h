@@ -180,13 +180,14 @@ struct PcgUpdArgs {
     int phase, kind, n1;
     long long ncol;
     double* partials;
-    int cpw;  // reserved (columns per warp), 1
+    int tile_rs;  // k_pcg_update_bj: shared-memory row stride (odd, >= n1)
 };
 __global__ void k_pcg_start(const double* g, double* r, double* d, long long n, double* partials,
                             PcgState* S);
-__global__ void k_pcg_hv(PcgHvArgs A, PcgState* S);
-__global__ void k_pcg_p(const double* __restrict__ z, const double* __restrict__ p_old,
-                        double* __restrict__ p_new, long long n, const PcgState* S);
+__global__ void k_pcg_hvp(PcgHvArgs A, PcgState* S);
+void launch_pcg_update_bj(epc_context* ctx, int cpw, int blocks, size_t smem, const PcgUpdArgs& U,
+                          PcgState* S);
+void set_pcg_update_bj_smem(int cpw, int bytes);
 __global__ void k_vec_differs(const double* a, const double* b, long long n, int* flag);
 __global__ void k_first_error(const int* col_err, long long ncol, int* out);
 __global__ void k_pcg_update(PcgUpdArgs A, PcgState* S);

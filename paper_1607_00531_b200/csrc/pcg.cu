@@ -7,11 +7,13 @@
 // reads the state once per chunk; kernels of iterations after convergence
 // (or after a curvature failure) return immediately.
 //
-// Per iteration: k_pcg_hv (p = z + beta p; q = H p; p.q; alpha = rz / pq)
-// and k_pcg_update (d += alpha p; r += (-alpha) q; z = M^{-1} r; r.r, r.z;
-// relres, relres_prec, stop test, beta = rz_new / rz). Element-wise work is
-// bitwise the reference's; the sweeps of the block-Jacobi solve run on lane
-// 0 from shared memory with the divisions lane-parallel in between.
+// Per iteration: k_pcg_hvp (p = z + beta p; q = H p; p.q; alpha = rz / pq)
+// and k_pcg_update_bj / k_pcg_update (d += alpha p; r += (-alpha) q;
+// z = M^{-1} r; r.r, r.z; relres, relres_prec, stop test, beta = rz_new /
+// rz). Element-wise work is bitwise the reference's. The block-Jacobi sweeps
+// run one lane per column over shared-memory tiles (k_pcg_update_bj);
+// k_pcg_update (one warp per column, lane-0 sweeps) serves the start phase
+// of the other preconditioners and the Jacobi / identity applies.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -119,6 +121,28 @@ __device__ __forceinline__ void ldlt_solve_warp(double* __restrict__ v, const do
     __syncwarp();
 }
 
+// The scalar end of an iteration (gn_pcg.cpp:105-108 for phase 0, :115-129):
+// rz / prec0 at the start; relres, relres_prec, the stop test and beta.
+__device__ void pcg_finish(PcgState* S, int phase, double srr, double srz) {
+    if (phase == 0) {
+        S->rz = srz;
+        S->prec0 = sqrt((srz < 0.0) ? 0.0 : srz);  // sqrt(std::max(rz, 0.0))
+    } else {
+        S->iters += 1;
+        S->relres = sqrt(srr) / S->gnorm;
+        S->relres_prec = S->prec0 > 0.0 ? sqrt((srz < 0.0) ? 0.0 : srz) / S->prec0 : 0.0;
+        if (S->relres <= S->eta) {
+            S->reached = 1;
+            S->done = 1;
+        } else {
+            S->beta = srz / S->rz;
+            S->rz = srz;
+            if (S->iters >= S->max_iters) S->done = 1;
+        }
+    }
+    S->cnt = 0;
+}
+
 }  // namespace
 
 // flag = (a != b) anywhere (values compared with ==, like std::vector's !=);
@@ -139,20 +163,6 @@ __global__ void k_first_error(const int* col_err, long long ncol, int* out) {
         if (col_err[c]) m = min(m, (int)c);
     m = warp_min_int(m);
     if ((threadIdx.x & 31) == 0 && m != 0x7fffffff) atomicMin(out, m);
-}
-
-// p_new = z (first iteration) or z + beta p_old (gn_pcg.cpp:128, applied at
-// the top of the next iteration); element-wise.
-__global__ void __launch_bounds__(256) k_pcg_p(const double* __restrict__ z,
-                                              const double* __restrict__ p_old,
-                                              double* __restrict__ p_new, long long n,
-                                              const PcgState* S) {
-    if (S->done) return;
-    const bool first = S->iters == 0;
-    const double beta = S->beta;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        p_new[i] = first ? z[i] : z[i] + beta * p_old[i];
 }
 
 // r = -g; gnorm = ||g||; zero-gradient short circuit (gn_pcg.cpp:96-103).
@@ -180,55 +190,6 @@ __global__ void __launch_bounds__(256) k_pcg_start(const double* g, double* r, d
             S->reached = 0;
             S->done = gnorm == 0.0 ? 1 : 0;
             if (gnorm == 0.0) S->reached = 1;
-            S->cnt = 0;
-        }
-    }
-}
-
-// q = H p with p = z (first iteration) or z + beta p_old, written to p_new;
-// partial p.q; the last block forms alpha = rz / pq (gn_pcg.cpp:110-114).
-// One block per column (j,k), threads along the contiguous column.
-__global__ void __launch_bounds__(128) k_pcg_hv(PcgHvArgs A, PcgState* S) {
-    __shared__ double sh[8];
-    if (S->done) return;
-    const int n1 = A.n1, m1 = A.m1, m2 = A.m2, m3 = A.m3;
-    const long long layer = (long long)n1 * m2;
-    const double* __restrict__ P = A.p_new;  // written by k_pcg_p
-    const double* __restrict__ D = A.diag;
-    const double* __restrict__ O = A.off;
-    double s = 0.0;
-    for (int c = blockIdx.x; c < A.ncol; c += gridDim.x) {
-        const int j = c % m2, k = c / m2;
-        const long long base = (long long)c * n1;
-        for (int i = threadIdx.x; i < n1; i += blockDim.x) {
-            const long long f = base + i;
-            const double x = P[f];
-            double acc = D[f] * x;
-            if (i > 0) acc += O[f - 1] * P[f - 1];
-            if (i < m1) acc += O[f] * P[f + 1];
-            double y = acc;
-            if (j > 0) y += A.w2 * (x - P[f - n1]);
-            if (j + 1 < m2) y += A.w2 * (x - P[f + n1]);
-            if (m3 > 1) {
-                if (k > 0) y += A.w3 * (x - P[f - layer]);
-                if (k + 1 < m3) y += A.w3 * (x - P[f + layer]);
-            }
-            A.q[f] = y;
-            s += x * y;
-        }
-    }
-    const double t = block_sum(s, sh);
-    if (threadIdx.x == 0) A.partials[blockIdx.x] = t;
-    if (arrive_last(&S->cnt)) {
-        __syncthreads();
-        const double pq = last_block_sum(A.partials, gridDim.x, 1, 0, sh);
-        if (threadIdx.x == 0) {
-            if (!(pq > 0.0)) {
-                S->err = 1;  // "pcg: nonpositive curvature encountered"
-                S->done = 1;
-            } else {
-                S->alpha = S->rz / pq;
-            }
             S->cnt = 0;
         }
     }
@@ -311,24 +272,210 @@ __global__ void __launch_bounds__(128) k_pcg_update(PcgUpdArgs A, PcgState* S) {
         const double srr = last_block_sum(A.partials, gridDim.x, 2, 0, sh);
         __syncthreads();
         const double srz = last_block_sum(A.partials, gridDim.x, 2, 1, sh);
+        if (threadIdx.x == 0) pcg_finish(S, A.phase, srr, srz);
+    }
+}
+
+// ---- fused p / Hessian apply, face-parallel ---------------------------------
+// p = z (first iteration) or z + beta p_old, then q = H p (GnHessian::apply,
+// objective.cpp:302-331) and the partial p.q; the last block forms alpha
+// (gn_pcg.cpp:110-114). The neighbours' p are recomputed from z and p_old
+// with the same operations, so they equal the stored p bit for bit; one
+// coalesced pass replaces k_pcg_p + k_pcg_hv (48 B/face instead of 56).
+// One face: neighbour indices are clamped so that every load is
+// unconditional (a load under a boundary branch cannot be hoisted, which
+// serialises the round trips); the boundary terms are then selected.
+template <bool FIRST>
+__device__ __forceinline__ void hvp_face(const PcgHvArgs& A, double beta, unsigned f, double& s) {
+    const double* __restrict__ Z = A.z;
+    const double* __restrict__ PO = A.p_old;
+    const unsigned n1 = A.n1, m1 = A.m1, m2 = A.m2, m3 = A.m3, layer = n1 * m2;
+    const unsigned c = f / n1, i = f - c * n1, k = c / m2, j = c - k * m2;
+    const bool bim = i > 0, bip = i < m1, bjm = j > 0, bjp = j + 1 < m2;
+    const bool bkm = m3 > 1 && k > 0, bkp = m3 > 1 && k + 1 < m3;
+    const unsigned fim = bim ? f - 1 : f, fip = bip ? f + 1 : f;
+    const unsigned fjm = bjm ? f - n1 : f, fjp = bjp ? f + n1 : f;
+    const unsigned fkm = bkm ? f - layer : f, fkp = bkp ? f + layer : f;
+    auto P = [&](unsigned g) { return FIRST ? __ldg(Z + g) : __ldg(Z + g) + beta * __ldg(PO + g); };
+    const double x = P(f), xim = P(fim), xip = P(fip), xjm = P(fjm), xjp = P(fjp);
+    const double xkm = P(fkm), xkp = P(fkp);
+    const double dg = __ldg(A.diag + f), oim = __ldg(A.off + fim), oi = __ldg(A.off + f);
+    A.p_new[f] = x;
+    double acc = dg * x;
+    if (bim) acc += oim * xim;
+    if (bip) acc += oi * xip;
+    double y = acc;
+    if (bjm) y += A.w2 * (x - xjm);
+    if (bjp) y += A.w2 * (x - xjp);
+    if (bkm) y += A.w3 * (x - xkm);
+    if (bkp) y += A.w3 * (x - xkp);
+    A.q[f] = y;
+    s += x * y;
+}
+
+template <bool FIRST>
+__device__ __forceinline__ double hvp_sweep(const PcgHvArgs& A, double beta) {
+    const unsigned n = A.n1 * A.m2 * A.m3;
+    const unsigned stride = gridDim.x * blockDim.x;
+    double s = 0.0;
+    unsigned f = blockIdx.x * blockDim.x + threadIdx.x;
+    for (; f + stride < n; f += 2 * stride) {
+        hvp_face<FIRST>(A, beta, f, s);
+        hvp_face<FIRST>(A, beta, f + stride, s);
+    }
+    if (f < n) hvp_face<FIRST>(A, beta, f, s);
+    return s;
+}
+
+__global__ void __launch_bounds__(256) k_pcg_hvp(PcgHvArgs A, PcgState* S) {
+    __shared__ double sh[8];
+    if (S->done) return;
+    const double s = S->iters == 0 ? hvp_sweep<true>(A, 0.0) : hvp_sweep<false>(A, S->beta);
+    const double t = block_sum(s, sh);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = t;
+    if (arrive_last(&S->cnt)) {
+        __syncthreads();
+        const double pq = last_block_sum(A.partials, gridDim.x, 1, 0, sh);
         if (threadIdx.x == 0) {
-            if (A.phase == 0) {
-                S->rz = srz;
-                S->prec0 = sqrt((srz < 0.0) ? 0.0 : srz);  // sqrt(std::max(rz, 0.0))
+            if (!(pq > 0.0)) {
+                S->err = 1;  // "pcg: nonpositive curvature encountered"
+                S->done = 1;
             } else {
-                S->iters += 1;
-                S->relres = sqrt(srr) / S->gnorm;
-                S->relres_prec = S->prec0 > 0.0 ? sqrt((srz < 0.0) ? 0.0 : srz) / S->prec0 : 0.0;
-                if (S->relres <= S->eta) {
-                    S->reached = 1;
-                    S->done = 1;
-                } else {
-                    S->beta = srz / S->rz;
-                    S->rz = srz;
-                    if (S->iters >= S->max_iters) S->done = 1;
-                }
+                S->alpha = S->rz / pq;
             }
             S->cnt = 0;
         }
+    }
+}
+
+// ---- block-Jacobi update, one thread per column in the sweeps ---------------
+// d += alpha p; r += (-alpha) q; z = (L D L^T)^{-1} r (TridiagFactor::
+// solve_column, operators.cpp:248-255); partial r.r and r.z. A block of
+// PCG_NT threads owns CPW consecutive columns, i.e. one contiguous span of
+// CPW * n1 faces, held whole in shared memory (r, then v, in X; l in Y; rows
+// of odd stride RS so the per-thread sweeps are bank-conflict free):
+//   1. all threads: coalesced flat pass over the span, element-wise updates
+//      of d and r (written back), r and l staged;
+//   2. thread cc < CPW: forward sweep v_i = r_i - l_{i-1} v_{i-1};
+//   3. all threads: v_i / d_i (d read coalesced from the factor);
+//   4. thread cc: backward sweep w_i = v_i - l_i w_{i+1};
+//   5. all threads: z written coalesced, partial r.z.
+// The sweeps do the operations of ldlt_solve_warp in the same order, so z
+// is bitwise the same; every global access is a flat coalesced pass.
+constexpr int PCG_NT = 256;
+template <int CPW, bool UPD>
+__global__ void __launch_bounds__(PCG_NT) k_pcg_update_bj(PcgUpdArgs A, PcgState* S) {
+    extern __shared__ __align__(16) double usm[];
+    __shared__ double sh[8];
+    if (S->done) return;
+    const int tid = threadIdx.x;
+    const int n1 = A.n1, RS = A.tile_rs;
+    const unsigned un1 = (unsigned)n1;
+    double* const X = usm;
+    double* const Y = X + CPW * RS;
+    const double a = S->alpha, ma = -a;
+    double* __restrict__ Dv = A.d;
+    double* __restrict__ Rv = A.r;
+    double* __restrict__ Zv = A.z;
+    const double* __restrict__ Pv = A.p;
+    const double* __restrict__ Qv = A.q;
+    const double* __restrict__ FD = A.fd;
+    const double* __restrict__ FL = A.fl;
+    const long long ngroups = (A.ncol + CPW - 1) / CPW;
+    double rr = 0.0, rz = 0.0;
+    for (long long gi = blockIdx.x; gi < ngroups; gi += gridDim.x) {
+        const long long c0 = gi * CPW;
+        const int nc = (int)(A.ncol - c0 < CPW ? A.ncol - c0 : CPW);
+        const size_t base = (size_t)c0 * n1;
+        const int ne = nc * n1;
+#pragma unroll 4
+        for (int e = tid; e < ne; e += PCG_NT) {
+            const size_t o = base + e;
+            const int cc = (int)((unsigned)e / un1), i = e - cc * n1;
+            double r = Rv[o];
+            if (UPD) {
+                const double dn = Dv[o] + a * Pv[o];
+                r += ma * Qv[o];
+                Dv[o] = dn;
+                Rv[o] = r;
+            }
+            rr += r * r;
+            X[cc * RS + i] = r;
+            Y[cc * RS + i] = FL[o];
+        }
+        __syncthreads();
+        if (tid < nc) {
+            double* x = X + tid * RS;
+            const double* y = Y + tid * RS;
+            double prev = x[0];
+#pragma unroll 4
+            for (int i = 1; i < n1; ++i) {
+                prev = x[i] - y[i - 1] * prev;
+                x[i] = prev;
+            }
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int e = tid; e < ne; e += PCG_NT) {
+            const int cc = (int)((unsigned)e / un1), i = e - cc * n1;
+            X[cc * RS + i] = X[cc * RS + i] / FD[base + e];
+        }
+        __syncthreads();
+        if (tid < nc) {
+            double* x = X + tid * RS;
+            const double* y = Y + tid * RS;
+            double nxt = x[n1 - 1];
+#pragma unroll 4
+            for (int i = n1 - 2; i >= 0; --i) {
+                nxt = x[i] - y[i] * nxt;
+                x[i] = nxt;
+            }
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int e = tid; e < ne; e += PCG_NT) {
+            const int cc = (int)((unsigned)e / un1), i = e - cc * n1;
+            const double zz = X[cc * RS + i];
+            Zv[base + e] = zz;
+            rz += Rv[base + e] * zz;
+        }
+        __syncthreads();
+    }
+    const double srr_b = block_sum(rr, sh);
+    __syncthreads();
+    const double srz_b = block_sum(rz, sh);
+    if (tid == 0) {
+        A.partials[(size_t)blockIdx.x * 2 + 0] = srr_b;
+        A.partials[(size_t)blockIdx.x * 2 + 1] = srz_b;
+    }
+    if (arrive_last(&S->cnt)) {
+        __syncthreads();
+        const double srr = last_block_sum(A.partials, gridDim.x, 2, 0, sh);
+        __syncthreads();
+        const double srz = last_block_sum(A.partials, gridDim.x, 2, 1, sh);
+        if (tid == 0) pcg_finish(S, A.phase, srr, srz);
+    }
+}
+
+void launch_pcg_update_bj(epc_context* ctx, int cpw, int blocks, size_t smem, const PcgUpdArgs& U,
+                          PcgState* S) {
+    const bool upd = U.phase == 1;
+    if (cpw == 8) {
+        if (upd) EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<8, true>), blocks, PCG_NT, smem, U, S);
+        else EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<8, false>), blocks, PCG_NT, smem, U, S);
+    } else {
+        if (upd) EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<16, true>), blocks, PCG_NT, smem, U, S);
+        else EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<16, false>), blocks, PCG_NT, smem, U, S);
+    }
+}
+
+void set_pcg_update_bj_smem(int cpw, int bytes) {
+    const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    if (cpw == 8) {
+        cudaFuncSetAttribute(k_pcg_update_bj<8, true>, attr, bytes);
+        cudaFuncSetAttribute(k_pcg_update_bj<8, false>, attr, bytes);
+    } else {
+        cudaFuncSetAttribute(k_pcg_update_bj<16, true>, attr, bytes);
+        cudaFuncSetAttribute(k_pcg_update_bj<16, false>, attr, bytes);
     }
 }

@@ -23,7 +23,7 @@ for kind, kname in ((0, "none"), (1, "jacobi"), (2, "block")):
     prof = ctx.profile_read()
     ctx.profile(False)
     line = [f"{kname:7s} iters={r['iters']:3d}"]
-    for k in ("pcg_p", "pcg_hv", "pcg_update"):
+    for k in ("pcg_hvp", "pcg_update"):
         ms, n = prof.get(k, (0.0, 1))
         us = ms / n * 1e3
         line.append(f"{k}={us:6.1f}us")
