@@ -188,6 +188,15 @@ __global__ void k_pcg_hvp(PcgHvArgs A, PcgState* S);
 void launch_pcg_update_bj(epc_context* ctx, int cpw, int blocks, size_t smem, const PcgUpdArgs& U,
                           PcgState* S);
 void set_pcg_update_bj_smem(int cpw, int bytes);
+struct PcgLoopArgs {
+    PcgHvArgs H;
+    PcgUpdArgs U;
+    double *pbuf0, *pbuf1;     // p alternates: iteration k writes pbuf[k & 1]
+    double *part_a, *part_b;   // per-block partials (p.q; r.r and r.z)
+    size_t part_cap;           // doubles available in each partials buffer
+    unsigned* bar;             // grid barrier counter, zeroed before the launch
+};
+bool launch_pcg_loop(epc_context* ctx, int cpw, size_t smem, const PcgLoopArgs& L, PcgState* S);
 __global__ void k_vec_differs(const double* a, const double* b, long long n, int* flag);
 __global__ void k_first_error(const int* col_err, long long ncol, int* out);
 __global__ void k_pcg_update(PcgUpdArgs A, PcgState* S);

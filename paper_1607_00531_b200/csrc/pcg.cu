@@ -285,7 +285,14 @@ __global__ void __launch_bounds__(128) k_pcg_update(PcgUpdArgs A, PcgState* S) {
 // One face: neighbour indices are clamped so that every load is
 // unconditional (a load under a boundary branch cannot be hoisted, which
 // serialises the round trips); the boundary terms are then selected.
-template <bool FIRST>
+// COH: z and p_old were written earlier in the same (persistent) kernel by
+// other blocks, so they are read with ld.global.cg (L2, no stale L1 line).
+template <bool COH>
+__device__ __forceinline__ double ld_vec(const double* p) {
+    return COH ? __ldcg(p) : __ldg(p);
+}
+
+template <bool FIRST, bool COH>
 __device__ __forceinline__ void hvp_face(const PcgHvArgs& A, double beta, unsigned f, double& s) {
     const double* __restrict__ Z = A.z;
     const double* __restrict__ PO = A.p_old;
@@ -296,7 +303,9 @@ __device__ __forceinline__ void hvp_face(const PcgHvArgs& A, double beta, unsign
     const unsigned fim = bim ? f - 1 : f, fip = bip ? f + 1 : f;
     const unsigned fjm = bjm ? f - n1 : f, fjp = bjp ? f + n1 : f;
     const unsigned fkm = bkm ? f - layer : f, fkp = bkp ? f + layer : f;
-    auto P = [&](unsigned g) { return FIRST ? __ldg(Z + g) : __ldg(Z + g) + beta * __ldg(PO + g); };
+    auto P = [&](unsigned g) {
+        return FIRST ? ld_vec<COH>(Z + g) : ld_vec<COH>(Z + g) + beta * ld_vec<COH>(PO + g);
+    };
     const double x = P(f), xim = P(fim), xip = P(fip), xjm = P(fjm), xjp = P(fjp);
     const double xkm = P(fkm), xkp = P(fkp);
     const double dg = __ldg(A.diag + f), oim = __ldg(A.off + fim), oi = __ldg(A.off + f);
@@ -313,24 +322,24 @@ __device__ __forceinline__ void hvp_face(const PcgHvArgs& A, double beta, unsign
     s += x * y;
 }
 
-template <bool FIRST>
+template <bool FIRST, bool COH>
 __device__ __forceinline__ double hvp_sweep(const PcgHvArgs& A, double beta) {
     const unsigned n = A.n1 * A.m2 * A.m3;
     const unsigned stride = gridDim.x * blockDim.x;
     double s = 0.0;
     unsigned f = blockIdx.x * blockDim.x + threadIdx.x;
     for (; f + stride < n; f += 2 * stride) {
-        hvp_face<FIRST>(A, beta, f, s);
-        hvp_face<FIRST>(A, beta, f + stride, s);
+        hvp_face<FIRST, COH>(A, beta, f, s);
+        hvp_face<FIRST, COH>(A, beta, f + stride, s);
     }
-    if (f < n) hvp_face<FIRST>(A, beta, f, s);
+    if (f < n) hvp_face<FIRST, COH>(A, beta, f, s);
     return s;
 }
 
 __global__ void __launch_bounds__(256) k_pcg_hvp(PcgHvArgs A, PcgState* S) {
     __shared__ double sh[8];
     if (S->done) return;
-    const double s = S->iters == 0 ? hvp_sweep<true>(A, 0.0) : hvp_sweep<false>(A, S->beta);
+    const double s = S->iters == 0 ? hvp_sweep<true, false>(A, 0.0) : hvp_sweep<false, false>(A, S->beta);
     const double t = block_sum(s, sh);
     if (threadIdx.x == 0) A.partials[blockIdx.x] = t;
     if (arrive_last(&S->cnt)) {
@@ -363,17 +372,26 @@ __global__ void __launch_bounds__(256) k_pcg_hvp(PcgHvArgs A, PcgState* S) {
 // The sweeps do the operations of ldlt_solve_warp in the same order, so z
 // is bitwise the same; every global access is a flat coalesced pass.
 constexpr int PCG_NT = 256;
-template <int CPW, bool UPD>
-__global__ void __launch_bounds__(PCG_NT) k_pcg_update_bj(PcgUpdArgs A, PcgState* S) {
-    extern __shared__ __align__(16) double usm[];
-    __shared__ double sh[8];
-    if (S->done) return;
+
+// One column group (steps 1-5 above) for the block; accumulates r.r, r.z.
+// COH: p and q come from other blocks of the same persistent kernel.
+template <bool COH>
+__device__ __forceinline__ double2 ld_vec2(const double* p) {
+    return COH ? __ldcg(reinterpret_cast<const double2*>(p)) : __ldg(reinterpret_cast<const double2*>(p));
+}
+
+// One column group (steps 1-5 above) for the block; accumulates r.r, r.z.
+// COH: p and q come from other blocks of the same persistent kernel. The
+// flat passes move two faces per thread (16-byte accesses): a group starts
+// at face c0 n1 with c0 a multiple of CPW (even), and the span nc n1 is even
+// unless nc is odd (the last group), whose final face goes scalar.
+template <int CPW, bool UPD, bool COH>
+__device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long long gi, double* X,
+                                         double* Y, double& rr, double& rz) {
     const int tid = threadIdx.x;
     const int n1 = A.n1, RS = A.tile_rs;
     const unsigned un1 = (unsigned)n1;
-    double* const X = usm;
-    double* const Y = X + CPW * RS;
-    const double a = S->alpha, ma = -a;
+    const double ma = -a;
     double* __restrict__ Dv = A.d;
     double* __restrict__ Rv = A.r;
     double* __restrict__ Zv = A.z;
@@ -381,70 +399,119 @@ __global__ void __launch_bounds__(PCG_NT) k_pcg_update_bj(PcgUpdArgs A, PcgState
     const double* __restrict__ Qv = A.q;
     const double* __restrict__ FD = A.fd;
     const double* __restrict__ FL = A.fl;
+    const long long c0 = gi * CPW;
+    const int nc = (int)(A.ncol - c0 < CPW ? A.ncol - c0 : CPW);
+    const size_t base = (size_t)c0 * n1;
+    const int ne = nc * n1;
+    const int ne2 = ne >> 1;
+    auto sidx = [&](int e) {
+        const int cc = (int)((unsigned)e / un1);
+        return cc * RS + (e - cc * n1);
+    };
+    auto stage1 = [&](int e, double r0, double l0) {
+        rr += r0 * r0;
+        const int k = sidx(e);
+        X[k] = r0;
+        Y[k] = l0;
+    };
+#pragma unroll 2
+    for (int h = tid; h < ne2; h += PCG_NT) {
+        const size_t o = base + 2 * (size_t)h;
+        double2 r = *reinterpret_cast<const double2*>(Rv + o);
+        if (UPD) {
+            const double2 pp = ld_vec2<COH>(Pv + o), qq = ld_vec2<COH>(Qv + o);
+            double2 dd = *reinterpret_cast<const double2*>(Dv + o);
+            dd.x = dd.x + a * pp.x;
+            dd.y = dd.y + a * pp.y;
+            r.x += ma * qq.x;
+            r.y += ma * qq.y;
+            *reinterpret_cast<double2*>(Dv + o) = dd;
+            *reinterpret_cast<double2*>(Rv + o) = r;
+        }
+        const double2 l = __ldg(reinterpret_cast<const double2*>(FL + o));
+        stage1(2 * h, r.x, l.x);
+        stage1(2 * h + 1, r.y, l.y);
+    }
+    if ((ne & 1) && tid == 0) {
+        const size_t o = base + ne - 1;
+        double r = Rv[o];
+        if (UPD) {
+            const double dn = Dv[o] + a * ld_vec<COH>(Pv + o);
+            r += ma * ld_vec<COH>(Qv + o);
+            Dv[o] = dn;
+            Rv[o] = r;
+        }
+        stage1(ne - 1, r, __ldg(FL + o));
+    }
+    __syncthreads();
+    if (tid < nc) {
+        double* x = X + tid * RS;
+        const double* y = Y + tid * RS;
+        double prev = x[0];
+#pragma unroll 4
+        for (int i = 1; i < n1; ++i) {
+            prev = x[i] - y[i - 1] * prev;
+            x[i] = prev;
+        }
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int h = tid; h < ne2; h += PCG_NT) {
+        const double2 dd = __ldg(reinterpret_cast<const double2*>(FD + base + 2 * (size_t)h));
+        const int k0 = sidx(2 * h), k1 = sidx(2 * h + 1);
+        X[k0] = X[k0] / dd.x;
+        X[k1] = X[k1] / dd.y;
+    }
+    if ((ne & 1) && tid == 0) {
+        const int k = sidx(ne - 1);
+        X[k] = X[k] / __ldg(FD + base + ne - 1);
+    }
+    __syncthreads();
+    if (tid < nc) {
+        double* x = X + tid * RS;
+        const double* y = Y + tid * RS;
+        double nxt = x[n1 - 1];
+#pragma unroll 4
+        for (int i = n1 - 2; i >= 0; --i) {
+            nxt = x[i] - y[i] * nxt;
+            x[i] = nxt;
+        }
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int h = tid; h < ne2; h += PCG_NT) {
+        const size_t o = base + 2 * (size_t)h;
+        const double2 r = *reinterpret_cast<const double2*>(Rv + o);
+        const double2 z = make_double2(X[sidx(2 * h)], X[sidx(2 * h + 1)]);
+        *reinterpret_cast<double2*>(Zv + o) = z;
+        rz += r.x * z.x;
+        rz += r.y * z.y;
+    }
+    if ((ne & 1) && tid == 0) {
+        const size_t o = base + ne - 1;
+        const double zz = X[sidx(ne - 1)];
+        Zv[o] = zz;
+        rz += Rv[o] * zz;
+    }
+    __syncthreads();
+}
+
+template <int CPW, bool UPD>
+__global__ void __launch_bounds__(PCG_NT) k_pcg_update_bj(PcgUpdArgs A, PcgState* S) {
+    extern __shared__ __align__(16) double usm[];
+    __shared__ double sh[8];
+    if (S->done) return;
+    double* const X = usm;
+    double* const Y = X + CPW * A.tile_rs;
+    const double a = S->alpha;
     const long long ngroups = (A.ncol + CPW - 1) / CPW;
     double rr = 0.0, rz = 0.0;
-    for (long long gi = blockIdx.x; gi < ngroups; gi += gridDim.x) {
-        const long long c0 = gi * CPW;
-        const int nc = (int)(A.ncol - c0 < CPW ? A.ncol - c0 : CPW);
-        const size_t base = (size_t)c0 * n1;
-        const int ne = nc * n1;
-#pragma unroll 4
-        for (int e = tid; e < ne; e += PCG_NT) {
-            const size_t o = base + e;
-            const int cc = (int)((unsigned)e / un1), i = e - cc * n1;
-            double r = Rv[o];
-            if (UPD) {
-                const double dn = Dv[o] + a * Pv[o];
-                r += ma * Qv[o];
-                Dv[o] = dn;
-                Rv[o] = r;
-            }
-            rr += r * r;
-            X[cc * RS + i] = r;
-            Y[cc * RS + i] = FL[o];
-        }
-        __syncthreads();
-        if (tid < nc) {
-            double* x = X + tid * RS;
-            const double* y = Y + tid * RS;
-            double prev = x[0];
-#pragma unroll 4
-            for (int i = 1; i < n1; ++i) {
-                prev = x[i] - y[i - 1] * prev;
-                x[i] = prev;
-            }
-        }
-        __syncthreads();
-#pragma unroll 4
-        for (int e = tid; e < ne; e += PCG_NT) {
-            const int cc = (int)((unsigned)e / un1), i = e - cc * n1;
-            X[cc * RS + i] = X[cc * RS + i] / FD[base + e];
-        }
-        __syncthreads();
-        if (tid < nc) {
-            double* x = X + tid * RS;
-            const double* y = Y + tid * RS;
-            double nxt = x[n1 - 1];
-#pragma unroll 4
-            for (int i = n1 - 2; i >= 0; --i) {
-                nxt = x[i] - y[i] * nxt;
-                x[i] = nxt;
-            }
-        }
-        __syncthreads();
-#pragma unroll 4
-        for (int e = tid; e < ne; e += PCG_NT) {
-            const int cc = (int)((unsigned)e / un1), i = e - cc * n1;
-            const double zz = X[cc * RS + i];
-            Zv[base + e] = zz;
-            rz += Rv[base + e] * zz;
-        }
-        __syncthreads();
-    }
+    for (long long gi = blockIdx.x; gi < ngroups; gi += gridDim.x)
+        bj_group<CPW, UPD, false>(A, a, gi, X, Y, rr, rz);
     const double srr_b = block_sum(rr, sh);
     __syncthreads();
     const double srz_b = block_sum(rz, sh);
-    if (tid == 0) {
+    if (threadIdx.x == 0) {
         A.partials[(size_t)blockIdx.x * 2 + 0] = srr_b;
         A.partials[(size_t)blockIdx.x * 2 + 1] = srz_b;
     }
@@ -453,8 +520,154 @@ __global__ void __launch_bounds__(PCG_NT) k_pcg_update_bj(PcgUpdArgs A, PcgState
         const double srr = last_block_sum(A.partials, gridDim.x, 2, 0, sh);
         __syncthreads();
         const double srz = last_block_sum(A.partials, gridDim.x, 2, 1, sh);
-        if (tid == 0) pcg_finish(S, A.phase, srr, srz);
+        if (threadIdx.x == 0) pcg_finish(S, A.phase, srr, srz);
     }
+}
+
+// ---- the whole PCG loop in one cooperative launch ---------------------------
+// Phase A (k_pcg_hvp's work) and phase B (k_pcg_update_bj's) alternate with
+// a grid barrier after each; every block then forms the same fixed-order sum
+// of the per-block partials and takes the same scalar decision (alpha; then
+// relres, the stop test and beta, gn_pcg.cpp:110-129), so no block waits on
+// a "last block". Block 0 publishes the final state. The barrier spin is
+// bounded: a block that waits > ~2 s marks S->err = 2 and leaves (no hang).
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ bool grid_barrier(unsigned* bar, unsigned& target) {
+    __shared__ int ok;
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        ok = 1;
+        const long long t0 = clock64();
+        while (ld_acquire_u32(bar) < target) {
+            __nanosleep(64);
+            if (clock64() - t0 > 4000000000LL) {
+                ok = 0;
+                break;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    return ok != 0;
+}
+
+// Fixed-order sum of n partials (stride, offset) by the whole block; the
+// same in every block (same order, same tree).
+__device__ double block_fixed_sum(const double* part, int n, int stride, int off, double* sh) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < n; b += blockDim.x) v += __ldcg(part + (size_t)b * stride + off);
+    const double t = block_sum(v, sh);
+    __shared__ double out;
+    if (threadIdx.x == 0) out = t;
+    __syncthreads();
+    return out;
+}
+
+template <int CPW>
+__global__ void __launch_bounds__(PCG_NT) k_pcg_loop(PcgLoopArgs L, PcgState* S) {
+    extern __shared__ __align__(16) double usm[];
+    __shared__ double sh[8];
+    double* const X = usm;
+    double* const Y = X + CPW * L.U.tile_rs;
+    // state after the start phase (identical in every block)
+    int iters = S->iters, done = S->done;
+    double rz = S->rz, beta = S->beta, alpha = S->alpha, relres = S->relres,
+           relres_prec = S->relres_prec;
+    const double gnorm = S->gnorm, prec0 = S->prec0, eta = S->eta;
+    const int max_iters = S->max_iters;
+    int reached = S->reached, err = 0;
+    unsigned target = 0;
+    const long long ngroups = (L.U.ncol + CPW - 1) / CPW;
+    for (int k = 0; !done; ++k) {
+        PcgHvArgs H = L.H;
+        H.p_new = (k & 1) ? L.pbuf1 : L.pbuf0;
+        H.p_old = (k & 1) ? L.pbuf0 : L.pbuf1;
+        const double s = iters == 0 ? hvp_sweep<true, true>(H, 0.0) : hvp_sweep<false, true>(H, beta);
+        const double sb = block_sum(s, sh);
+        if (threadIdx.x == 0) L.part_a[blockIdx.x] = sb;
+        if (!grid_barrier(L.bar, target)) {
+            err = 2;
+            break;
+        }
+        const double pq = block_fixed_sum(L.part_a, gridDim.x, 1, 0, sh);
+        if (!(pq > 0.0)) {
+            err = 1;  // "pcg: nonpositive curvature encountered"
+            break;
+        }
+        alpha = rz / pq;
+        PcgUpdArgs U = L.U;
+        U.p = H.p_new;
+        double rr = 0.0, rzp = 0.0;
+        for (long long gi = blockIdx.x; gi < ngroups; gi += gridDim.x)
+            bj_group<CPW, true, true>(U, alpha, gi, X, Y, rr, rzp);
+        const double srr_b = block_sum(rr, sh);
+        __syncthreads();
+        const double srz_b = block_sum(rzp, sh);
+        if (threadIdx.x == 0) {
+            L.part_b[(size_t)blockIdx.x * 2 + 0] = srr_b;
+            L.part_b[(size_t)blockIdx.x * 2 + 1] = srz_b;
+        }
+        if (!grid_barrier(L.bar, target)) {
+            err = 2;
+            break;
+        }
+        const double srr = block_fixed_sum(L.part_b, gridDim.x, 2, 0, sh);
+        const double srz = block_fixed_sum(L.part_b, gridDim.x, 2, 1, sh);
+        iters += 1;
+        relres = sqrt(srr) / gnorm;
+        relres_prec = prec0 > 0.0 ? sqrt((srz < 0.0) ? 0.0 : srz) / prec0 : 0.0;
+        if (relres <= eta) {
+            reached = 1;
+            done = 1;
+        } else {
+            beta = srz / rz;
+            rz = srz;
+            if (iters >= max_iters) done = 1;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        S->iters = iters;
+        S->rz = rz;
+        S->beta = beta;
+        S->alpha = alpha;
+        S->relres = relres;
+        S->relres_prec = relres_prec;
+        S->reached = reached;
+        S->err = err;
+        S->done = 1;
+    }
+}
+
+// Cooperative launch of the loop; false when the device cannot hold the grid.
+bool launch_pcg_loop(epc_context* ctx, int cpw, size_t smem, const PcgLoopArgs& L, PcgState* S) {
+    const void* fn = cpw == 8 ? (const void*)k_pcg_loop<8> : (const void*)k_pcg_loop<16>;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return false;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, PCG_NT, smem) != cudaSuccess || per_sm < 1)
+        return false;
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+    if (!coop) return false;
+    const int blocks = ctx->num_sms * per_sm;
+    if ((size_t)blocks * 2 + 8 > L.part_cap) return false;
+    PcgLoopArgs La = L;
+    PcgState* Sa = S;
+    void* args[] = {&La, &Sa};
+    cudaEvent_t ev0 = nullptr;
+    if (ctx->profiling) epc_prof_begin(ctx, "pcg_loop", &ev0);
+    const cudaError_t e = cudaLaunchCooperativeKernel(fn, blocks, PCG_NT, args, smem, ctx->stream);
+    ctx->launches++;
+    if (ctx->profiling) epc_prof_end(ctx, "pcg_loop", ev0);
+    return e == cudaSuccess;
 }
 
 void launch_pcg_update_bj(epc_context* ctx, int cpw, int blocks, size_t smem, const PcgUpdArgs& U,
