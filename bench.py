@@ -278,13 +278,17 @@ def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
     world = dist.get_world_size() if dist is not None else 1
     # per-kernel times of one profiled solve; algorithmic bytes per face per
     # launch: pcg_hvp reads z, p_old, diag, off and writes p, q
-    # (48 B); pcg_update reads d, r, p, q, fd, fl and writes d, r, z (72 B)
+    # (48 B); pcg_update reads d, r, p, q, fd, fl and writes d, r, z (72 B).
+    # The profiled solve is one solve; npcg counts a.steps solves.
     ctx.profile(True)
     ctx.profile_reset()
     solve_device()
     prof = ctx.profile_read()
     ctx.profile(False)
     per_face = {"pcg_update": 72, "pcg_hvp": 48}
+    # the persistent loop kernel runs both phases (120 B/face per PCG
+    # iteration) for all iterations of one PCG solve per launch
+    loop_iters = npcg / a.steps / max(1, prof.get("pcg_loop", (0, 0))[1])
     kernels = []
     for name, (ms, n) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
         if not n:
@@ -294,7 +298,23 @@ def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
         if name in per_face:
             gbs = per_face[name] * g.faces / (ms / n / 1e3) / 1e9
             k.update(alg_bytes=per_face[name] * g.faces, achieved_gbs=gbs)
+        elif name == "pcg_loop":
+            alg = 120 * g.faces * loop_iters
+            k.update(alg_bytes=alg, pcg_iterations_per_launch=loop_iters,
+                     achieved_gbs=alg / (ms / n / 1e3) / 1e9)
         kernels.append(k)
+    roof = None
+    top = next((k for k in kernels if "achieved_gbs" in k), None)
+    if top is not None:
+        try:
+            peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+            src = "measured"
+        except Exception:
+            peak, src = 6650.0, "fallback"
+        roof = {"bound": "hbm", "kernel": top["kernel"], "achieved": top["achieved_gbs"], "peak": peak,
+                "peak_source": src, "unit": "GB/s", "frac": top["achieved_gbs"] / peak, "traffic": None,
+                "note": "algorithmic bytes (120 B/face per PCG iteration) / CUDA-event time; "
+                        "C2 vectors are 8.5 MB, so launch ramp and grid barriers weigh"}
     out = {"metric": f"voxel-iterations/s (GN-PCG, {'x'.join(map(str, g.dims()))}, fp64)",
            "value": g.faces * npcg / t_dev * world, "unit": GN_UNIT,
            "time_to_solution_s": t_dev / a.steps, "pcg_iterations_per_solve": npcg // a.steps,
@@ -302,7 +322,7 @@ def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
            "e2e": {"value": g.faces * npcg_h / t_e2e * world, "unit": GN_UNIT,
                    "h2d_bytes_per_step": (2 * g.cells + g.faces) * 8,
                    "d2h_bytes_per_step": g.faces * 8},
-           "gpu_launches": launches, "kernels": kernels[:8],
+           "gpu_launches": launches, "roofline": roof, "kernels": kernels[:8],
            "l2": "256 MB flush write before every timed step; the C2 PCG vectors (~85 MB) "
                  "fit in L2 within a solve"}
     if rank == 0 and not a.no_cpu_baseline:
