@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gn", action="store_true", help="skip the GN-PCG leg (configs[1])")
     ap.add_argument("--gn-config", default="C2")
+    ap.add_argument("--no-f32", action="store_true", help="skip the fp32-variant leg")
     return ap.parse_args()
 
 
@@ -336,6 +337,57 @@ def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
     return out
 
 
+def run_f32_leg(a, ctx, dev, stream, flush, g, ipn, imn, iters, b64, dist):
+    """fp32 variant (BASELINE configs[2] "fp64 and an fp32 variant"), reported
+    separately: the same solve through epc_admm_solve_f32, device-resident
+    throughput, e2e with host float32 buffers, and its deviation from the
+    fp64 result (which is bitwise the reference's) on the same inputs."""
+    import torch
+    cfg = abi.AdmmConfig(max_iter=iters, eps_abs=1e-300, eps_rel=1e-300)
+    ip32 = np.ascontiguousarray(ipn[:g.cells], dtype=np.float32)
+    im32 = np.ascontiguousarray(imn[:g.cells], dtype=np.float32)
+    ip_d, im_d = torch.from_numpy(ip32).to(dev), torch.from_numpy(im32).to(dev)
+    ip_h, im_h = torch.from_numpy(ip32).pin_memory(), torch.from_numpy(im32).pin_memory()
+    torch.cuda.synchronize(dev)
+
+    def timed(fn, k):
+        tot, launches, out = 0.0, 0, None
+        for _ in range(k):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ctx.reset_launch_count()
+            e0.record(stream)
+            out = fn()
+            e1.record(stream)
+            e1.synchronize()
+            launches += ctx.launch_count()
+            tot += e0.elapsed_time(e1) / 1e3
+        return tot, launches, out
+
+    for _ in range(a.warmup):
+        ctx.admm_solve_f32(g, ip_d, im_d, cfg=cfg)
+    t_dev, launches, r = timed(lambda: ctx.admm_solve_f32(g, ip_d, im_d, cfg=cfg), a.steps)
+    t_e2e, _, rh = timed(lambda: ctx.admm_solve_f32(g, ip_h.numpy(), im_h.numpy(), cfg=cfg), a.steps)
+    from paper_1607_00531_b200 import shard
+    t_dev = shard.max_over_ranks(t_dev, dist, dev)
+    t_e2e = shard.max_over_ranks(t_e2e, dist, dev)
+    world = dist.get_world_size() if dist is not None else 1
+    b32 = r["b"].double().cpu().numpy()
+    ref = np.asarray(b64, dtype=np.float64)
+    units = g.faces * iters * a.steps * world
+    return {"metric": f"voxel-iterations/s (ADMM fp32 variant, {'x'.join(map(str, g.dims()))})",
+            "value": units / t_dev, "unit": UNIT, "ms_per_step": t_dev / a.steps * 1e3,
+            "dtype": "f32", "time_to_solution_s": t_dev / a.steps,
+            "e2e": {"value": units / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * g.cells * 4,
+                    "d2h_bytes_per_step": 3 * g.faces * 4},
+            "gpu_launches": launches,
+            "rel_l2_b_vs_fp64": float(np.linalg.norm(b32 - ref) / max(np.linalg.norm(ref), 1e-300)),
+            "note": "fp32 storage and element arithmetic, fp64-accumulated sums, thresholds "
+                    "rescaled for fp32; not bitwise (tolerance in tests/test_gpu_admm_f32.py)"}
+
+
 def run_slabs(a, iters):
     """C5: one volume, k-slabs across the ranks; strong scaling.
     Each rank generates the same seeded volume and keeps its slab; the solve
@@ -559,9 +611,10 @@ def main():
     # roofline: per-kernel CUDA-event timing of one profiled solve
     ctx.profile(True)
     ctx.profile_reset()
-    solve_device()
+    r_last = solve_device()
     prof = ctx.profile_read()
     ctx.profile(False)
+    last_b = r_last["b"][:g.faces].double().cpu().numpy() if a.config != "C4" else None
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -631,6 +684,9 @@ def main():
     gn = None
     if not a.no_gn and a.config != "C4":
         gn = run_gn_leg(a, ctx, dev, stream, flush, rank, dist)
+    f32 = None
+    if not a.no_f32 and a.config != "C4":
+        f32 = run_f32_leg(a, ctx, dev, stream, flush, g, ipn, imn, iters, last_b, dist)
 
     if rank == 0:
         line = {"metric": metric_for(a.config), "value": value, "unit": UNIT, "n_gpus": world,
@@ -651,6 +707,8 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu}
         if gn is not None:
             line["gn"] = gn
+        if f32 is not None:
+            line["fp32"] = f32
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

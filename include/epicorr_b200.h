@@ -287,6 +287,18 @@ int epc_residual(epc_context* ctx, const epc_grid* g, int mem, const double* ipl
                  const double* iminus, const double* b, double* r);
 
 /* Library build identity (arch, mode) for logs. */
+/* fp32 variant of admm_solve (BASELINE configs[2] "fp64 and an fp32 variant";
+ * SURVEY 8(d)): the same algorithm with fp32 storage and element arithmetic,
+ * sums accumulated in fp64, QP/SQP thresholds rescaled for fp32 (admm_f32.cu).
+ * Not bitwise: its deviation from the fp64 reference is stated in DESIGN.md.
+ * Arrays are float32 (cells for the images, faces for b, z, u); NULL starts
+ * are zero; rows/status as epc_admm_solve. */
+int epc_admm_solve_f32(epc_context* ctx, const epc_grid* g, int mem, const float* iplus,
+                       const float* iminus, const float* b0, const float* z0, const float* u0,
+                       float* b_out, float* z_out, float* u_out, double* rho,
+                       const epc_objective_params* p, const epc_admm_config* cfg, int level_tag,
+                       epc_admm_row* rows, int max_rows, epc_solve_status* status);
+
 const char* epc_build_info(void);
 
 /* ---- either side of the solve (image.hpp:62-86) -------- */

@@ -22,6 +22,7 @@ EXPORTS = [
     "epc_context_create", "epc_context_destroy", "epc_set_stream", "epc_last_error",
     "epc_set_mode", "epc_profile_enable", "epc_profile_read", "epc_profile_reset",
     "epc_launch_count", "epc_reset_launch_count", "epc_admm_solve", "epc_admm_solve_batch",
+    "epc_admm_solve_f32",
     "epc_b_update", "epc_z_update", "epc_dct_solve", "epc_dual_update",
     "epc_augmented_lagrangian", "epc_rho_schedule", "epc_qp_active_set_batch", "epc_gn_solve",
     "epc_objective_gn", "epc_gn_hessian_build", "epc_gn_hessian_apply", "epc_precond_apply",
@@ -72,6 +73,8 @@ def _declare(L):
     L.epc_reset_launch_count.restype = None
     L.epc_admm_solve.argtypes = [X, G, C.c_int, X, X, X, X, X, X, X, X, dptr, P, A, C.c_int,
                                  C.POINTER(AdmmRow), C.c_int, C.POINTER(SolveStatus)]
+    L.epc_admm_solve_f32.argtypes = [X, G, C.c_int, X, X, X, X, X, X, X, X, dptr, P, A, C.c_int,
+                                     X, C.c_int, X]
     L.epc_admm_solve_batch.argtypes = [X, G, C.c_int, C.c_int, X, X, X, X, X, X, X, X, dptr, P, A,
                                        C.c_int, C.POINTER(AdmmRow), C.c_int, C.POINTER(SolveStatus)]
     L.epc_b_update.argtypes = [X, G, C.c_int, X, X, X, X, X, C.c_double, P, A, X,

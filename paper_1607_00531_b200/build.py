@@ -17,11 +17,17 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libepicorr_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["api.cu", "bstep.cu", "zstep.cu", "aux_kernels.cu", "gn.cu", "pcg.cu", "slab.cu", "multilevel.cu", "image.cu"]
+SOURCES = ["api.cu", "bstep.cu", "zstep.cu", "aux_kernels.cu", "gn.cu", "pcg.cu", "slab.cu", "multilevel.cu", "image.cu",
+           "admm_f32.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-prec-div=true", "-prec-sqrt=true",
          "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-rdc=false", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
+
+
+# the fp32 variant has no bitwise contract: contraction to FMA is allowed there
+FMAD_ON = {"admm_f32.cu"}
+LIBS = ["-lcudart", "-lcublas"]
 
 
 def _stale(target, deps):
@@ -41,7 +47,10 @@ def _compile(src, verbose):
     deps = [os.path.join(CSRC, src)] + _headers()
     if not _stale(out, deps):
         return out
-    cmd = [NVCC, *ARCH, *FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-c",
+    flags = [f for f in FLAGS if not (src in FMAD_ON and f == "-fmad=false")]
+    if src in FMAD_ON:
+        flags.append("-fmad=true")
+    cmd = [NVCC, *ARCH, *flags, "-Xptxas", "-v" if verbose else "-O3", "-c",
            os.path.join(CSRC, src), "-o", out]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -62,7 +71,7 @@ def build(verbose=False, force=False):
     with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     if _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, *LIBS]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

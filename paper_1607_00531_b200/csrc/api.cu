@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include <cublas_v2.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -99,6 +101,8 @@ enum Slot {
     S_X0, S_X1, S_X2, S_X3,
     S_SL0, S_SL1,
     S_ML0, S_ML1, S_MLI, S_MLD, S_MLB, S_MLO, S_MLIP, S_MLIM, S_MLFIP, S_MLFIM,
+    S_F32_IP, S_F32_IM, S_F32_B0, S_F32_B1, S_F32_Z0, S_F32_Z1, S_F32_U0, S_F32_U1, S_F32_T0,
+    S_F32_T1, S_F32_MATS, S_F32_Q, S_F32_S, S_F32_COL, S_F32_SCAL, S_F32_PART,
     S_COUNT
 };
 
@@ -854,6 +858,7 @@ void epc_context_destroy(epc_context* ctx) {
         cudaEventDestroy(pe.stop);
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -1201,4 +1206,5 @@ const char* epc_build_info(void) {
 #include "slab_host.inc"
 #include "multilevel_host.inc"
 #include "image_host.inc"
+#include "admm_f32_host.inc"
 

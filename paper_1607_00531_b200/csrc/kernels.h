@@ -241,3 +241,34 @@ __global__ void k_add(double* x, const double* n, long long len);
 __global__ void k_image_sums(const double* a, const double* b, long long n, int pass, double ma,
                              double mb, double* partials);
 __global__ void k_swap_axes(const double* in, double* out, int d0, int d1, int d2, int a, int b);
+
+// ---- fp32 ADMM variant (admm_f32.cu) ----------------------------------------
+struct BStepF32Params {
+    const float *ip, *im, *b, *z, *u;
+    float* b_out;
+    int m1, n1;
+    long long ncol;
+    float h, inv_h, o1, V, rho, alpha, sqp_tol_rel;
+    int sqp_max, qp_cap, check_kkt;
+    unsigned long long* counter;
+    float *qscr, *sscr;  // per-CTA scratch: Schur rows (m1 x n1) and matrix (m1 x m1)
+    long long qstride, sstride;
+    float* col_kkt;
+    double *col_sr, *col_sd;
+    int* col_err;
+    long long* col_work;  // sqp << 40 | qp << 16 | max_active
+};
+size_t bstep_f32_smem_bytes(int n1);
+int bstep_f32_slots_per_sm(size_t smem);
+void launch_bstep_f32(epc_context* ctx, int slots, size_t smem, const BStepF32Params& P);
+void launch_reduce_f32cols(epc_context* ctx, const BStepF32Params& P, long long ncol, double* od,
+                           long long* oi);
+void launch_rhs_f32(epc_context* ctx, int blocks, const float* b, const float* u, float w, float* out,
+                    long long n);
+void launch_div_f32(epc_context* ctx, int blocks, float* x, const float* lam23, float aV, float rV,
+                    int n1, long long n);
+void launch_dual_f32(epc_context* ctx, int blocks, const float* b, const float* z, const float* zo,
+                     const float* u, float* un, int n1, int m2, int m3, float ih2, float ih3,
+                     long long n, double* part);
+void launch_scale_f32(epc_context* ctx, int blocks, float* x, float a, long long n);
+void launch_d2f(epc_context* ctx, int blocks, const double* a, float* b, long long n);

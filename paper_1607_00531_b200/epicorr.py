@@ -170,6 +170,42 @@ class Context:
         return dict(b=bo, z=zo, u=uo, rho=r.value, stop=st.stop, message=st.message.decode(),
                     rows=abi.rows_to_dicts(rows, min(st.nrows, cfg.max_iter)))
 
+    @staticmethod
+    def _ptr32(a):
+        if a is None:
+            return None
+        if _is_dev(a):
+            assert str(a.dtype) == "torch.float32" and a.is_contiguous()
+            return C.c_void_p(a.data_ptr())
+        assert isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags["C_CONTIGUOUS"]
+        return C.c_void_p(a.ctypes.data)
+
+    def admm_solve_f32(self, g: Grid, ip, im, b=None, z=None, u=None, rho=0.0, params=None,
+                       cfg=None, level_tag=0):
+        """fp32 variant of admm_solve (epc_admm_solve_f32; not bitwise).
+        ip/im/b/z/u: float32 numpy arrays or CUDA tensors. Returns the admm_solve dict."""
+        params = params or ObjectiveParams()
+        cfg = cfg or AdmmConfig()
+        mem = self._mem(ip, im, b, z, u)
+        nf = g.faces
+        if _is_dev(ip):
+            import torch
+            bo, zo, uo = (torch.empty(nf, dtype=torch.float32, device=ip.device) for _ in range(3))
+        else:
+            bo, zo, uo = (np.zeros(nf, dtype=np.float32) for _ in range(3))
+        rows = (AdmmRow * max(cfg.max_iter, 1))()
+        st = SolveStatus()
+        r = C.c_double(rho)
+        P32 = self._ptr32
+        rc = self.lib.epc_admm_solve_f32(self.h, C.byref(g), mem, P32(ip), P32(im), P32(b), P32(z),
+                                         P32(u), P32(bo), P32(zo), P32(uo), C.byref(r),
+                                         C.byref(params), C.byref(cfg), level_tag, rows,
+                                         cfg.max_iter, C.byref(st))
+        if rc != 0:
+            _raise(rc, st.message.decode() or self._err())
+        return dict(b=bo, z=zo, u=uo, rho=r.value, stop=st.stop, message=st.message.decode(),
+                    rows=abi.rows_to_dicts(rows, min(st.nrows, cfg.max_iter)))
+
     def admm_solve_batch(self, g: Grid, npairs, ip, im, rho=None, params=None, cfg=None,
                          level_tag=0):
         params = params or ObjectiveParams()
