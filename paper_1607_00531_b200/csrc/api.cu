@@ -103,6 +103,7 @@ enum Slot {
     S_ML0, S_ML1, S_MLI, S_MLD, S_MLB, S_MLO, S_MLIP, S_MLIM, S_MLFIP, S_MLFIM,
     S_F32_IP, S_F32_IM, S_F32_B0, S_F32_B1, S_F32_Z0, S_F32_Z1, S_F32_U0, S_F32_U1, S_F32_T0,
     S_F32_T1, S_F32_MATS, S_F32_Q, S_F32_S, S_F32_COL, S_F32_SCAL, S_F32_PART,
+    S_CTIME,
     S_COUNT
 };
 
@@ -358,7 +359,10 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
     const size_t smem = bstep_smem_bytes(g.n1);
     if (smem > ctx->smem_optin) fail(EPC_ERR_UNSUPPORTED, "column too long for shared memory");
     const HDiv hd = make_hdiv(g.h1);
-    const bool diag = (ctx->mode & (EPC_MODE_BSTEP_TIMING | EPC_MODE_BSTEP_CHAINED)) != 0;
+    // EPC_BSTEP_TAIL (dev aid): per-CTA exit times and per-column durations,
+    // recorded by the diagnostic instantiation only
+    static const bool tail = getenv("EPC_BSTEP_TAIL") != nullptr;
+    const bool diag = tail || (ctx->mode & (EPC_MODE_BSTEP_TIMING | EPC_MODE_BSTEP_CHAINED)) != 0;
 #ifdef EPC_FORCE_DIAG
     const bool diag_forced = true;
 #else
@@ -418,7 +422,60 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
     P.total_cols = total;
     P.timing = (ctx->mode & EPC_MODE_BSTEP_TIMING) ? slot_t<long long>(ctx, S_GN9, 28) : nullptr;
     P.cert = (ctx->mode & EPC_MODE_BSTEP_CHAINED) ? 0 : 1;
+    if (tail && total < (1LL << 31)) P.col_ns = slot_t<unsigned>(ctx, S_CTIME, (size_t)total);
+    P.cta_span = tail ? slot_t<unsigned long long>(ctx, S_GN8, (size_t)slots * 2) : nullptr;
     EPC_LAUNCH(ctx, "admm_bstep", kern, (unsigned)slots, 32, smem, P);
+    if (tail) {
+        std::vector<unsigned long long> t((size_t)slots * 2);
+        CK(cudaMemcpyAsync(t.data(), P.cta_span, t.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        const unsigned long long t0 = *std::min_element(t.begin(), t.begin() + slots);
+        std::vector<double> e;
+        for (int k = 0; k < (int)slots; ++k) e.push_back((t[slots + k] - t0) * 1e-6);
+        std::sort(e.begin(), e.end());
+        double idle = 0.0;
+        for (double x : e) idle += e.back() - x;
+        std::fprintf(stderr, "bstep tail: first exit %.3f ms, median %.3f, p90 %.3f, last %.3f; idle %.1f%%\n",
+                     e.front(), e[e.size() / 2], e[e.size() * 9 / 10], e.back(),
+                     100.0 * idle / (e.back() * e.size()));
+        if (P.col_ns) {
+            std::vector<unsigned> ns((size_t)total);
+            std::vector<int> ci((size_t)total * 4);
+            CK(cudaMemcpyAsync(ns.data(), P.col_ns, total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaMemcpyAsync(ci.data(), col_i, total * 16, cudaMemcpyDeviceToHost, ctx->stream));
+            sync(ctx);
+            std::vector<long long> idx((size_t)total);
+            for (long long k = 0; k < total; ++k) idx[k] = k;
+            std::partial_sort(idx.begin(), idx.begin() + 5, idx.end(), [&](long long a, long long b) { return ns[a] > ns[b]; });
+            double mean = 0;
+            for (unsigned v : ns) mean += v;
+            mean /= total;
+            std::fprintf(stderr, "  column ns mean %.0f; slowest:", mean);
+            for (int k = 0; k < 5; ++k) {
+                const long long c = idx[k];
+                std::fprintf(stderr, " [col %lld %.3f ms sqp %d qp %d act %d]", c, ns[c] * 1e-6, ci[total + c],
+                             ci[2 * total + c], ci[3 * total + c]);
+            }
+            std::fprintf(stderr, "\n");
+            static std::vector<unsigned> prev;
+            if (prev.size() == ns.size()) {
+                long long heavy = 0, was = 0;
+                double sx = 0, sy = 0, sxx = 0, syy = 0, sxy = 0;
+                for (long long k = 0; k < total; ++k) {
+                    const double x = std::log((double)prev[k] + 1), y = std::log((double)ns[k] + 1);
+                    sx += x; sy += y; sxx += x * x; syy += y * y; sxy += x * y;
+                    if (ns[k] > 1000000u) {
+                        ++heavy;
+                        if (prev[k] > 500000u) ++was;
+                    }
+                }
+                const double n = (double)total;
+                const double r = (sxy - sx * sy / n) / std::sqrt((sxx - sx * sx / n) * (syy - sy * sy / n));
+                std::fprintf(stderr, "  predictability: corr(log ns) %.3f; columns > 1 ms: %lld, of which > 0.5 ms before: %lld\n", r, heavy, was);
+            }
+            prev = ns;
+        }
+    }
     check_launch();
     return BStepRun{col_i, col_d};
 }

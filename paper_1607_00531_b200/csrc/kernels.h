@@ -28,6 +28,8 @@ struct BStepParams {
     long long total_cols;
     long long* timing;  // optional [16]: phase cycles [0..9] (lane 0), counters [10..15]
     int cert;           // 1: decide SQP / line-search tests on certified enclosures
+    unsigned long long* cta_span;  // optional [2 x grid]: %globaltimer at CTA start / exit (dev aid)
+    unsigned* col_ns;   // optional: each column's duration in ns (dev aid, EPC_BSTEP_TAIL)
 };
 // DH = HPow2 | HGen (model.cuh); DIAG: phase timing / counters and the
 // chained mode compiled in (diagnostic instantiation, selected by ctx->mode)

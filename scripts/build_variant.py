@@ -16,7 +16,10 @@ os.makedirs(out, exist_ok=True)
 
 def cc(src):
     o = os.path.join(out, f"{name}_{os.path.splitext(src)[0]}.o")
-    cmd = [B.NVCC, *B.ARCH, *B.FLAGS, *defs, "-c", os.path.join(B.CSRC, src), "-o", o]
+    flags = [f for f in B.FLAGS if not (src in B.FMAD_ON and f == "-fmad=false")]
+    if src in B.FMAD_ON:
+        flags.append("-fmad=true")
+    cmd = [B.NVCC, *B.ARCH, *flags, *defs, "-c", os.path.join(B.CSRC, src), "-o", o]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         raise SystemExit(r.stderr)
@@ -26,5 +29,5 @@ def cc(src):
 with ThreadPoolExecutor(len(B.SOURCES)) as ex:
     objs = list(ex.map(cc, B.SOURCES))
 lib = os.path.join(out, f"{name}.so")
-subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", lib, *objs, "-lcudart"], check=True)
+subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", lib, *objs, *B.LIBS], check=True)
 print(lib)
