@@ -90,14 +90,17 @@ __device__ __forceinline__ float cell_r(const BStepF32Params& P, const float* ip
 // LDL^T of the tridiagonal G (lane 0); false on a nonpositive pivot. fp32
 // keeps the pivot reciprocals (rd = 1/d): the sweeps are then FMA chains
 // and the factor's chain is one reciprocal, not an IEEE division, per step.
-__device__ bool factor_f(const float* gd, const float* go, float* rd, float* fl, int n) {
+__device__ bool factor_f(const float* __restrict__ gd, const float* __restrict__ go,
+                         float* __restrict__ rd, float* __restrict__ fl, int n) {
     float prev = gd[0];
     bool ok = prev > 0.0f;
     float r = __frcp_rn(prev);
     rd[0] = r;
+#pragma unroll 8
     for (int i = 1; i < n; ++i) {
-        const float l = go[i - 1] * r;
-        const float d = gd[i] - l * go[i - 1];
+        const float o = go[i - 1];
+        const float l = o * r;
+        const float d = gd[i] - l * o;
         r = __frcp_rn(d);
         fl[i - 1] = l;
         rd[i] = r;
@@ -106,15 +109,19 @@ __device__ bool factor_f(const float* gd, const float* go, float* rd, float* fl,
     fl[n - 1] = 0.0f;
     return ok;
 }
-// ColFactor::solve (admm.cpp:56-60), one thread, any (generic) memory
-__device__ void solve_f(float* x, const float* rd, const float* fl, int n) {
+// ColFactor::solve (admm.cpp:56-60), one thread, any (generic) memory; the
+// unrolled loops let the operand loads run ahead of the FMA chain
+__device__ void solve_f(float* __restrict__ x, const float* __restrict__ rd,
+                        const float* __restrict__ fl, int n) {
     float prev = x[0];
+#pragma unroll 8
     for (int i = 1; i < n; ++i) {
         prev = x[i] - fl[i - 1] * prev;
         x[i] = prev;
     }
     float nxt = x[n - 1] * rd[n - 1];
     x[n - 1] = nxt;
+#pragma unroll 8
     for (int i = n - 2; i >= 0; --i) {
         nxt = x[i] * rd[i] - fl[i] * nxt;
         x[i] = nxt;

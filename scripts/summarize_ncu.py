@@ -35,7 +35,7 @@ def capture(src, dst):
     out = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(out.splitlines()))
-    h, u, v = r[0], r[1], r[2]
+    h, u = r[0], r[1]
     keys = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum",
             "dram__bytes_write.sum", "launch__grid_size", "launch__block_size",
             "launch__registers_per_thread", "launch__occupancy_limit_shared_mem",
@@ -43,23 +43,27 @@ def capture(src, dst):
             "smsp__issue_active.avg.pct_of_peak_sustained_active",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
             "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"]
-    d = {}
-    for k in keys:
-        if k in h:
-            i = h.index(k)
-            d[k] = [v[i], u[i]]
-    stalls = {}
-    for i, n in enumerate(h):
-        if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued"):
-            try:
-                x = float(v[i].replace(",", ""))
-            except ValueError:
-                continue
-            if x > 0:
-                stalls[n.replace("smsp__pcsamp_warps_issue_stalled_", "")] = x
-    t = sum(stalls.values()) or 1.0
-    d["stall_mix_pct"] = {k: round(100 * x / t, 1) for k, x in
-                          sorted(stalls.items(), key=lambda kv: -kv[1])}
+    out_list = []
+    for v in r[2:]:
+        d = {}
+        for k in keys:
+            if k in h:
+                i = h.index(k)
+                d[k] = [v[i], u[i]]
+        stalls = {}
+        for i, n in enumerate(h):
+            if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued"):
+                try:
+                    x = float(v[i].replace(",", ""))
+                except ValueError:
+                    continue
+                if x > 0:
+                    stalls[n.replace("smsp__pcsamp_warps_issue_stalled_", "")] = x
+        t = sum(stalls.values()) or 1.0
+        d["stall_mix_pct"] = {k: round(100 * x / t, 1) for k, x in
+                              sorted(stalls.items(), key=lambda kv: -kv[1])}
+        out_list.append(d)
+    d = out_list[0] if len(out_list) == 1 else out_list  # one capture: a dict (bench reads it)
     json.dump(d, open(dst, "w"), indent=1)
 
 
