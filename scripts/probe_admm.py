@@ -16,6 +16,7 @@ ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--check", type=int, default=0, help="oracle iterations to compare (0 = skip)")
 ap.add_argument("--prod", action="store_true", help="production kernel (no phase timing)")
+ap.add_argument("--no-kkt", action="store_true", help="check_kkt = false (cost of the KKT check)")
 a = ap.parse_args()
 
 t = time.time()
@@ -23,6 +24,8 @@ d = synth.make_config(a.config, scale=a.scale)
 print(f"generate {a.config}: {time.time() - t:.2f}s faces={d.grid.faces}", flush=True)
 ctx = Context(0)
 cfg = abi.AdmmConfig(max_iter=a.iters, eps_abs=1e-300, eps_rel=1e-300)
+if a.no_kkt:
+    cfg.check_kkt = 0
 r = ctx.admm_solve(d.grid, d.iplus, d.iminus, cfg=abi.AdmmConfig(max_iter=2, eps_abs=1e-300, eps_rel=1e-300))
 ctx.set_mode(0 if a.prod else 1)
 ctx.profile(True)
