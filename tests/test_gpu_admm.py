@@ -85,6 +85,27 @@ def test_admm_solve_small_bitwise(ctx, oracle, scale):
             assert a[k] == pytest.approx(r[k], rel=1e-12, abs=1e-300), k
 
 
+@pytest.mark.parametrize("m,h,scale", [((512, 6, 4), (1.0, 1.0, 1.0), 1.0),
+                                       ((512, 6, 4), (1.0, 1.0, 1.0), 400.0),
+                                       ((301, 5, 3), (0.7, 1.3, 0.9), 1.0)])
+def test_admm_solve_long_columns_bitwise(ctx, oracle, m, h, scale):
+    """Long phase-encoding columns (n1 = 513 as in C5, and an odd n1 with a
+    non-power-of-two h1, i.e. the exact-division path): the b-step's shared-
+    memory layout, its chain helpers and every certified shortcut against the
+    oracle, bitwise."""
+    d = synth.make_pair(synth.SynthSpec(m=m, seed=13))
+    g = abi.Grid.make(*m, h=h)  # the spacing only rescales the same arrays
+    ip, im = d.iplus * scale, d.iminus * scale
+    cfg = abi.AdmmConfig(max_iter=8, **EXACT)
+    ref = oracle.admm_solve(g, ip, im, cfg=cfg)
+    out = ctx.admm_solve(g, ip, im, cfg=cfg)
+    assert out["stop"] == ref["stop"] and len(out["rows"]) == len(ref["rows"])
+    for k in ("b", "z", "u"):
+        assert np.array_equal(out[k], ref[k]), k
+    for a, r in zip(out["rows"], ref["rows"]):
+        assert a["rho"] == r["rho"] and a["kkt_violation"] == r["kkt_violation"]
+
+
 def test_admm_solve_default_tolerances_stop_early(ctx, oracle):
     g, ip, im = small_pair()
     ref = oracle.admm_solve(g, ip, im)
