@@ -287,6 +287,32 @@ int epc_residual(epc_context* ctx, const epc_grid* g, int mem, const double* ipl
                  const double* iminus, const double* b, double* r);
 
 /* Library build identity (arch, mode) for logs. */
+/* The reference's test-side helpers of the path, bitwise:
+ * avg_x1 / diff_x1 (faces -> cells) and diff_x1_adjoint (cells -> faces),
+ * operators.hpp:25-32; smoother_hessian_apply, operators.hpp:43;
+ * TridiagBlocks::apply (y += s T x), operators.hpp:61; tridiag_solve_batched
+ * (nonpositive pivot: EPC_ERR_RUNTIME naming the column), operators.hpp:80;
+ * DctCoupledSolver::apply (Gt z), operators.hpp:102;
+ * DistanceEval::hessian_apply at b (V Jr^T Jr p), objective.hpp:57;
+ * is_strictly_feasible (max |D1 b| <= 1 - 1e-10), objective.hpp:46. */
+int epc_avg_x1(epc_context* ctx, const epc_grid* g, int mem, const double* b, double* out);
+int epc_diff_x1(epc_context* ctx, const epc_grid* g, int mem, const double* b, double* out);
+int epc_diff_x1_adjoint(epc_context* ctx, const epc_grid* g, int mem, const double* r,
+                        double* out);
+int epc_smoother_hessian_apply(epc_context* ctx, const epc_grid* g, int mem, const double* b,
+                               double* out);
+int epc_tridiag_apply(epc_context* ctx, const epc_grid* g, int mem, const double* diag,
+                      const double* off, const double* x, double s, double* y);
+int epc_tridiag_solve_batched(epc_context* ctx, const epc_grid* g, int mem, const double* diag,
+                              const double* off, const double* rhs, double* x);
+int epc_dct_apply(epc_context* ctx, const epc_grid* g, int mem, const double* z, double alpha,
+                  double rho, double* out);
+int epc_distance_hessian_apply(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
+                               const double* iminus, const double* b, const double* p,
+                               double* out);
+int epc_is_strictly_feasible(epc_context* ctx, const epc_grid* g, int mem, const double* b,
+                             int* feasible);
+
 /* fp32 variant of admm_solve (BASELINE configs[2] "fp64 and an fp32 variant";
  * SURVEY 8(d)): the same algorithm with fp32 storage and element arithmetic,
  * sums accumulated in fp64, QP/SQP thresholds rescaled for fp32 (admm_f32.cu).

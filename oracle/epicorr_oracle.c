@@ -2439,3 +2439,160 @@ int oracle_simulate_pair(const epc_grid* gg, const double* truth, const double* 
     }
     return EPC_OK;
 }
+
+/* ======================================================================
+ * The reference's test-side helpers of the path
+ * ====================================================================== */
+
+/* avg_x1, operators.cpp:27-37 */
+int oracle_avg_x1(const epc_grid* gg, const double* b, double* out) {
+    G g;
+    int rc = grid_make(gg, &g, NULL, 0);
+    if (rc) return rc;
+    for (long long c = 0; c < g.ncol; ++c)
+        for (int i = 0; i < g.m1; ++i)
+            out[c * g.m1 + i] = 0.5 * (b[c * g.n1 + i] + b[c * g.n1 + i + 1]);
+    return EPC_OK;
+}
+
+/* diff_x1, operators.cpp:40-52 */
+int oracle_diff_x1(const epc_grid* gg, const double* b, double* out) {
+    G g;
+    int rc = grid_make(gg, &g, NULL, 0);
+    if (rc) return rc;
+    const double ih = 1.0 / g.h1;
+    for (long long c = 0; c < g.ncol; ++c)
+        for (int i = 0; i < g.m1; ++i)
+            out[c * g.m1 + i] = (b[c * g.n1 + i + 1] - b[c * g.n1 + i]) * ih;
+    return EPC_OK;
+}
+
+/* diff_x1_adjoint, operators.cpp:54-68 */
+int oracle_diff_x1_adjoint(const epc_grid* gg, const double* r, double* out) {
+    G g;
+    int rc = grid_make(gg, &g, NULL, 0);
+    if (rc) return rc;
+    const double ih = 1.0 / g.h1;
+    const int m1 = g.m1, n1 = g.n1;
+    for (long long c = 0; c < g.ncol; ++c) {
+        const double* rc_ = r + c * m1;
+        double* oc = out + c * n1;
+        oc[0] = -rc_[0] * ih;
+        for (int i = 1; i < m1; ++i) oc[i] = (rc_[i - 1] - rc_[i]) * ih;
+        oc[m1] = rc_[m1 - 1] * ih;
+    }
+    return EPC_OK;
+}
+
+int oracle_smoother_hessian_apply(const epc_grid* gg, const double* b, double* out) {
+    G g;
+    int rc = grid_make(gg, &g, NULL, 0);
+    if (rc) return rc;
+    smoother_hessian_apply(&g, b, out);
+    return EPC_OK;
+}
+
+/* TridiagBlocks::apply, operators.cpp:202-216: y += s T x */
+int oracle_tridiag_apply(const epc_grid* gg, const double* diag, const double* off,
+                         const double* x, double s, double* y) {
+    G g;
+    int rc = grid_make(gg, &g, NULL, 0);
+    if (rc) return rc;
+    const int m1 = g.m1, n1 = g.n1;
+    for (long long c = 0; c < g.ncol; ++c) {
+        const double* xc = x + c * n1;
+        const double* d = diag + c * n1;
+        const double* o = off + c * n1;
+        double* yc = y + c * n1;
+        for (int i = 0; i <= m1; ++i) {
+            double acc = d[i] * xc[i];
+            if (i > 0) acc += o[i - 1] * xc[i - 1];
+            if (i < m1) acc += o[i] * xc[i + 1];
+            yc[i] += s * acc;
+        }
+    }
+    return EPC_OK;
+}
+
+/* tridiag_solve_batched, operators.cpp:264-273 (factorize, then solve) */
+int oracle_tridiag_solve_batched(const epc_grid* gg, const double* diag, const double* off,
+                                 const double* rhs, double* x, char* msg, size_t msglen) {
+    G g;
+    int rc = grid_make(gg, &g, msg, msglen);
+    if (rc) return rc;
+    double *fd = dalloc(g.nface), *fl = dalloc(g.nface);
+    rc = tridiag_factorize(&g, diag, off, fd, fl, msg, msglen);
+    if (rc == EPC_OK) {
+        memcpy(x, rhs, sizeof(double) * (size_t)g.nface);
+        tridiag_solve(&g, fd, fl, x);
+    }
+    free(fd);
+    free(fl);
+    return rc;
+}
+
+/* DctCoupledSolver::apply, operators.cpp:420-446 */
+int oracle_dct_apply(const epc_grid* gg, const double* z, double alpha, double rho, double* out) {
+    G g;
+    int rc = grid_make(gg, &g, NULL, 0);
+    if (rc) return rc;
+    const double V = g.V;
+    const int n1 = g.n1, m2 = g.m2, m3 = g.m3;
+    const double w2 = alpha * V / (g.h2 * g.h2);
+    const double w3 = alpha * V / (g.h3 * g.h3);
+    const long long layer = (long long)n1 * m2;
+    for (long long c = 0; c < g.ncol; ++c) {
+        const int j = (int)(c % m2), k = (int)(c / m2);
+        const double* zc = z + c * n1;
+        double* oc = out + c * n1;
+        for (int i = 0; i < n1; ++i) oc[i] = rho * V * zc[i];
+        if (j > 0)
+            for (int i = 0; i < n1; ++i) oc[i] += w2 * (zc[i] - zc[i - n1]);
+        if (j + 1 < m2)
+            for (int i = 0; i < n1; ++i) oc[i] += w2 * (zc[i] - zc[i + n1]);
+        if (m3 > 1) {
+            if (k > 0)
+                for (int i = 0; i < n1; ++i) oc[i] += w3 * (zc[i] - zc[i - layer]);
+            if (k + 1 < m3)
+                for (int i = 0; i < n1; ++i) oc[i] += w3 * (zc[i] - zc[i + layer]);
+        }
+    }
+    return EPC_OK;
+}
+
+/* DistanceEval::hessian_apply (objective.cpp:128-147) with jac_lo / jac_hi
+ * of distance() at b (objective.cpp:93-126, residual_column) */
+int oracle_distance_hessian_apply(const epc_grid* gg, const double* iplus, const double* iminus,
+                                  const double* b, const double* p, double* out) {
+    G g;
+    int rc = grid_make(gg, &g, NULL, 0);
+    if (rc) return rc;
+    const int m1 = g.m1, n1 = g.n1;
+    const double V = g.V;
+    double *r = dalloc(m1), *jlo = dalloc(m1), *jhi = dalloc(m1);
+    memset(out, 0, sizeof(double) * (size_t)g.nface);
+    for (long long c = 0; c < g.ncol; ++c) {
+        Interp ip = column_of(&g, iplus, c), im = column_of(&g, iminus, c);
+        residual_column(&ip, &im, &g, b + c * n1, r, jlo, jhi);
+        const double* pc = p + c * n1;
+        double* oc = out + c * n1;
+        for (int i = 0; i < m1; ++i) {
+            const double jp = jlo[i] * pc[i] + jhi[i] * pc[i + 1];
+            oc[i] += V * jlo[i] * jp;
+            oc[i + 1] += V * jhi[i] * jp;
+        }
+    }
+    free(r);
+    free(jlo);
+    free(jhi);
+    return EPC_OK;
+}
+
+/* is_strictly_feasible, objective.cpp:35-37: 1 / 0, or a negative error */
+int oracle_is_strictly_feasible(const epc_grid* gg, const double* b) {
+    G g;
+    int rc = grid_make(gg, &g, NULL, 0);
+    if (rc) return -rc;
+    return d1_norm_inf(&g, b) <= 1.0 - 1e-10 ? 1 : 0;
+}
+

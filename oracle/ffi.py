@@ -104,6 +104,14 @@ class Checker:
         L.oracle_ncc.argtypes = [G, dptr, dptr, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
         L.oracle_simulate_pair.argtypes = [G, dptr, dptr, C.c_double, C.c_ulonglong, C.c_double,
                                            dptr, dptr, C.c_char_p, C.c_size_t]
+        for nm in ("oracle_avg_x1", "oracle_diff_x1", "oracle_diff_x1_adjoint",
+                   "oracle_smoother_hessian_apply"):
+            getattr(L, nm).argtypes = [G, dptr, dptr]
+        L.oracle_tridiag_apply.argtypes = [G, dptr, dptr, dptr, C.c_double, dptr]
+        L.oracle_tridiag_solve_batched.argtypes = [G, dptr, dptr, dptr, dptr, C.c_char_p, C.c_size_t]
+        L.oracle_dct_apply.argtypes = [G, dptr, C.c_double, C.c_double, dptr]
+        L.oracle_distance_hessian_apply.argtypes = [G, dptr, dptr, dptr, dptr, dptr]
+        L.oracle_is_strictly_feasible.argtypes = [G, dptr]
         if hasattr(L, "oracle_write_volume"):  # reference harness only
             L.oracle_write_volume.argtypes = [C.c_char_p, G, C.c_int, dptr, C.c_char_p, C.c_size_t]
             L.oracle_read_volume.argtypes = [C.c_char_p, G, IP, dptr, C.c_longlong,
@@ -249,6 +257,57 @@ class Checker:
                     reached_tol=bool(res.reached_tol), message=msg.value.decode())
 
     # ---- image.cpp: correct_pair, ssd, ncc, simulate_pair -------------------------
+    # ---- the reference's test-side helpers of the path ----
+    def avg_x1(self, g, b):
+        out = np.zeros(g.cells)
+        assert self.lib.oracle_avg_x1(C.byref(g), _p(b), _p(out)) == 0
+        return out
+
+    def diff_x1(self, g, b):
+        out = np.zeros(g.cells)
+        assert self.lib.oracle_diff_x1(C.byref(g), _p(b), _p(out)) == 0
+        return out
+
+    def diff_x1_adjoint(self, g, r):
+        out = np.zeros(g.faces)
+        assert self.lib.oracle_diff_x1_adjoint(C.byref(g), _p(r), _p(out)) == 0
+        return out
+
+    def smoother_hessian_apply(self, g, b):
+        out = np.zeros(g.faces)
+        assert self.lib.oracle_smoother_hessian_apply(C.byref(g), _p(b), _p(out)) == 0
+        return out
+
+    def tridiag_apply(self, g, diag, off, x, s, y):
+        y = np.array(y, dtype=np.float64)
+        assert self.lib.oracle_tridiag_apply(C.byref(g), _p(diag), _p(off), _p(x), s, _p(y)) == 0
+        return y
+
+    def tridiag_solve_batched(self, g, diag, off, rhs):
+        x = np.zeros(g.faces)
+        msg = C.create_string_buffer(256)
+        rc = self.lib.oracle_tridiag_solve_batched(C.byref(g), _p(diag), _p(off), _p(rhs), _p(x),
+                                                   msg, 256)
+        if rc:
+            raise RuntimeError(msg.value.decode())
+        return x
+
+    def dct_apply(self, g, z, alpha, rho):
+        out = np.zeros(g.faces)
+        assert self.lib.oracle_dct_apply(C.byref(g), _p(z), alpha, rho, _p(out)) == 0
+        return out
+
+    def distance_hessian_apply(self, g, ip, im, b, p):
+        out = np.zeros(g.faces)
+        assert self.lib.oracle_distance_hessian_apply(C.byref(g), _p(ip), _p(im), _p(b), _p(p),
+                                                      _p(out)) == 0
+        return out
+
+    def is_strictly_feasible(self, g, b):
+        r = self.lib.oracle_is_strictly_feasible(C.byref(g), _p(b))
+        assert r >= 0
+        return bool(r)
+
     def correct_pair(self, g, ip, im, b):
         cp, cm = np.zeros(g.cells), np.zeros(g.cells)
         msg = C.create_string_buffer(256)

@@ -116,6 +116,20 @@ int oracle_simulate_pair(const epc_grid* g, const double* truth, const double* b
                          double noise_sigma, unsigned long long seed, double feas_margin,
                          double* out_plus, double* out_minus, char* msg, size_t msglen);
 
+/* the reference's test-side helpers of the path */
+int oracle_avg_x1(const epc_grid* g, const double* b, double* out);
+int oracle_diff_x1(const epc_grid* g, const double* b, double* out);
+int oracle_diff_x1_adjoint(const epc_grid* g, const double* r, double* out);
+int oracle_smoother_hessian_apply(const epc_grid* g, const double* b, double* out);
+int oracle_tridiag_apply(const epc_grid* g, const double* diag, const double* off,
+                         const double* x, double s, double* y);
+int oracle_tridiag_solve_batched(const epc_grid* g, const double* diag, const double* off,
+                                 const double* rhs, double* x, char* msg, size_t msglen);
+int oracle_dct_apply(const epc_grid* g, const double* z, double alpha, double rho, double* out);
+int oracle_distance_hessian_apply(const epc_grid* g, const double* iplus, const double* iminus,
+                                  const double* b, const double* p, double* out);
+int oracle_is_strictly_feasible(const epc_grid* g, const double* b);
+
 #ifdef __cplusplus
 }
 #endif

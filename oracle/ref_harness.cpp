@@ -11,6 +11,7 @@
 #include <exception>
 #include <stdexcept>
 #include <string>
+#include <span>
 #include <vector>
 
 #include "epicorr/admm.hpp"
@@ -564,6 +565,97 @@ int oracle_unpermute_field(const epc_grid* gg, int pe_axis, const double* in, do
         *kind = int(vd.kind);
         std::memcpy(out, vd.v.data(), sizeof(double) * vd.v.size());
     });
+}
+
+
+// ---- the reference's test-side helpers of the path ----
+namespace {
+CellField cellfield(const GridSpec& g, const double* v) {
+    CellField c(g);
+    c.v.assign(v, v + g.cells());
+    return c;
+}
+TridiagBlocks blocks(const GridSpec& g, const double* diag, const double* off) {
+    TridiagBlocks t(g);
+    t.diag.assign(diag, diag + g.faces());
+    t.off.assign(off, off + g.faces());
+    return t;
+}
+}  // namespace
+
+int oracle_avg_x1(const epc_grid* gg, const double* b, double* out) {
+    return guarded(nullptr, 0, [&] {
+        const GridSpec g = to_grid(gg);
+        const CellField c = avg_x1(faces(g, b));
+        std::memcpy(out, c.v.data(), sizeof(double) * c.v.size());
+    });
+}
+
+int oracle_diff_x1(const epc_grid* gg, const double* b, double* out) {
+    return guarded(nullptr, 0, [&] {
+        const GridSpec g = to_grid(gg);
+        const CellField c = diff_x1(faces(g, b));
+        std::memcpy(out, c.v.data(), sizeof(double) * c.v.size());
+    });
+}
+
+int oracle_diff_x1_adjoint(const epc_grid* gg, const double* r, double* out) {
+    return guarded(nullptr, 0, [&] {
+        const GridSpec g = to_grid(gg);
+        copy_out(diff_x1_adjoint(cellfield(g, r)), out);
+    });
+}
+
+int oracle_smoother_hessian_apply(const epc_grid* gg, const double* b, double* out) {
+    return guarded(nullptr, 0, [&] {
+        const GridSpec g = to_grid(gg);
+        copy_out(smoother_hessian_apply(faces(g, b), g_threads), out);
+    });
+}
+
+int oracle_tridiag_apply(const epc_grid* gg, const double* diag, const double* off,
+                         const double* x, double s, double* y) {
+    return guarded(nullptr, 0, [&] {
+        const GridSpec g = to_grid(gg);
+        const TridiagBlocks t = blocks(g, diag, off);
+        const std::size_t n = std::size_t(g.faces());
+        t.apply(std::span<const double>(x, n), std::span<double>(y, n), s);
+    });
+}
+
+int oracle_tridiag_solve_batched(const epc_grid* gg, const double* diag, const double* off,
+                                 const double* rhs, double* x, char* msg, size_t msglen) {
+    return guarded(msg, msglen, [&] {
+        const GridSpec g = to_grid(gg);
+        copy_out(tridiag_solve_batched(blocks(g, diag, off), faces(g, rhs), g_threads), x);
+    });
+}
+
+int oracle_dct_apply(const epc_grid* gg, const double* z, double alpha, double rho, double* out) {
+    return guarded(nullptr, 0, [&] {
+        const GridSpec g = to_grid(gg);
+        const DctCoupledSolver solver(g, g_threads);
+        copy_out(solver.apply(faces(g, z), alpha, rho), out);
+    });
+}
+
+int oracle_distance_hessian_apply(const epc_grid* gg, const double* iplus, const double* iminus,
+                                  const double* b, const double* p, double* out) {
+    return guarded(nullptr, 0, [&] {
+        const GridSpec g = to_grid(gg);
+        const VolumePair pair(cells(g, iplus), cells(g, iminus));
+        const DistanceEval de = distance(pair, faces(g, b), g_threads);
+        copy_out(de.hessian_apply(faces(g, p), g_threads), out);
+    });
+}
+
+int oracle_is_strictly_feasible(const epc_grid* gg, const double* b) {
+    int res = 0;
+    const int rc = guarded(nullptr, 0, [&] {
+        const GridSpec g = to_grid(gg);
+        res = is_strictly_feasible(faces(g, b)) ? 1 : 0;
+    });
+    return rc ? -rc : res;
 }
 
 } // extern "C"

@@ -31,7 +31,9 @@ EXPORTS = [
     "epc_slab_zdiff", "epc_slab_scale", "epc_gnslab_objective", "epc_gnslab_hessian",
     "epc_gnslab_hv", "epc_gnslab_update", "epc_gnslab_axpy", "epc_gnslab_negate",
     "epc_gnslab_dot", "epc_default_schedule", "epc_restrict_image", "epc_prolong_field",
-    "epc_multilevel_solve", "epc_correct_pair", "epc_ssd", "epc_ncc", "epc_simulate_pair", "epc_write_volume", "epc_read_volume",
+    "epc_multilevel_solve", "epc_avg_x1", "epc_diff_x1", "epc_diff_x1_adjoint",
+    "epc_smoother_hessian_apply", "epc_tridiag_apply", "epc_tridiag_solve_batched", "epc_dct_apply",
+    "epc_distance_hessian_apply", "epc_is_strictly_feasible", "epc_correct_pair", "epc_ssd", "epc_ncc", "epc_simulate_pair", "epc_write_volume", "epc_read_volume",
     "epc_permute_to_axis1", "epc_unpermute_field",
 ]
 
@@ -119,6 +121,13 @@ def _declare(L):
     L.epc_default_schedule.argtypes = [G, I, I, GA, I, IPT]
     L.epc_restrict_image.argtypes = [X, G, G, I, X, X]
     L.epc_prolong_field.argtypes = [X, G, G, I, X, X]
+    for nm in ("epc_avg_x1", "epc_diff_x1", "epc_diff_x1_adjoint", "epc_smoother_hessian_apply"):
+        getattr(L, nm).argtypes = [X, G, I, X, X]
+    L.epc_tridiag_apply.argtypes = [X, G, I, X, X, X, C.c_double, X]
+    L.epc_tridiag_solve_batched.argtypes = [X, G, I, X, X, X, X]
+    L.epc_dct_apply.argtypes = [X, G, I, X, C.c_double, C.c_double, X]
+    L.epc_distance_hessian_apply.argtypes = [X, G, I, X, X, X, X, X]
+    L.epc_is_strictly_feasible.argtypes = [X, G, I, X, IPT]
     L.epc_correct_pair.argtypes = [X, G, I, X, X, X, X, X]
     L.epc_ssd.argtypes = [X, G, I, X, X, D]
     L.epc_ncc.argtypes = [X, G, I, X, X, D]

@@ -18,7 +18,7 @@ OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libepicorr_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["api.cu", "bstep.cu", "zstep.cu", "aux_kernels.cu", "gn.cu", "pcg.cu", "slab.cu", "multilevel.cu", "image.cu",
-           "admm_f32.cu"]
+           "admm_f32.cu", "operators_t2.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-prec-div=true", "-prec-sqrt=true",
          "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-rdc=false", "--expt-relaxed-constexpr",

@@ -1264,4 +1264,5 @@ const char* epc_build_info(void) {
 #include "multilevel_host.inc"
 #include "image_host.inc"
 #include "admm_f32_host.inc"
+#include "t2_host.inc"
 

@@ -274,3 +274,22 @@ void launch_dual_f32(epc_context* ctx, int blocks, const float* b, const float* 
                      long long n, double* part);
 void launch_scale_f32(epc_context* ctx, int blocks, float* x, float a, long long n);
 void launch_d2f(epc_context* ctx, int blocks, const double* a, float* b, long long n);
+
+// ---- the reference's test-side helpers (operators_t2.cu) ----
+void launch_avg_x1(epc_context* ctx, const double* b, int m1, long long ncell, double* out);
+void launch_diff_x1(epc_context* ctx, const double* b, int m1, long long ncell, double ih,
+                    double* out);
+void launch_diff_x1_adjoint(epc_context* ctx, const double* r, int m1, long long nface, double ih,
+                            double* out);
+void launch_smoother_apply(epc_context* ctx, const double* b, int m1, int m2, int m3,
+                           long long nface, double w1, double w2, double w3, double* out);
+void launch_tridiag_apply(epc_context* ctx, const double* d, const double* o, const double* x,
+                          int m1, long long nface, double s, double* y);
+void launch_tridiag_solve_cols(epc_context* ctx, const double* d, const double* o, double* fd,
+                               double* fl, double* x, int n1, long long ncol, long long* bad);
+void launch_dct_apply(epc_context* ctx, const double* z, int n1, int m2, int m3, long long nface,
+                      double rv, double w2, double w3, double* out);
+void launch_distance_hv(epc_context* ctx, const double* jlo, const double* jhi, const double* p,
+                        int m1, long long nface, double V, double* out);
+int launch_d1_absmax(epc_context* ctx, const double* b, int m1, long long ncell, double ih,
+                     double* part);

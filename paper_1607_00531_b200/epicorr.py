@@ -325,6 +325,69 @@ class Context:
         return dict(b=bo, stop=st.stop, message=st.message.decode(),
                     rows=abi.rows_to_dicts(rows, min(st.nrows, cfg.max_outer + 1)))
 
+    # ---- the reference's test-side helpers of the path ---------
+    def _unary(self, fn, g, a, n_out):
+        mem = self._mem(a)
+        out = self._like(a, n_out)
+        self._check(getattr(self.lib, fn)(self.h, C.byref(g), mem, self._ptr(a), self._ptr(out)))
+        return out
+
+    def avg_x1(self, g, b):
+        """avg_x1 (operators.cpp:27-37): faces -> cells."""
+        return self._unary("epc_avg_x1", g, b, g.cells)
+
+    def diff_x1(self, g, b):
+        """diff_x1 (operators.cpp:40-52): faces -> cells."""
+        return self._unary("epc_diff_x1", g, b, g.cells)
+
+    def diff_x1_adjoint(self, g, r):
+        """diff_x1_adjoint (operators.cpp:54-68): cells -> faces."""
+        return self._unary("epc_diff_x1_adjoint", g, r, g.faces)
+
+    def smoother_hessian_apply(self, g, b):
+        """smoother_hessian_apply (operators.cpp:141-183)."""
+        return self._unary("epc_smoother_hessian_apply", g, b, g.faces)
+
+    def tridiag_apply(self, g, diag, off, x, s, y):
+        """TridiagBlocks::apply (operators.cpp:202-216): returns y + s T x."""
+        mem = self._mem(diag, off, x, y)
+        yo = y.clone() if _is_dev(y) else np.array(y, dtype=np.float64)
+        self._check(self.lib.epc_tridiag_apply(self.h, C.byref(g), mem, self._ptr(diag),
+                                               self._ptr(off), self._ptr(x), s, self._ptr(yo)))
+        return yo
+
+    def tridiag_solve_batched(self, g, diag, off, rhs):
+        """tridiag_solve_batched (operators.cpp:264-273)."""
+        mem = self._mem(diag, off, rhs)
+        x = self._like(rhs, g.faces)
+        self._check(self.lib.epc_tridiag_solve_batched(self.h, C.byref(g), mem, self._ptr(diag),
+                                                       self._ptr(off), self._ptr(rhs), self._ptr(x)))
+        return x
+
+    def dct_apply(self, g, z, alpha, rho):
+        """DctCoupledSolver::apply (operators.cpp:420-446): Gt z."""
+        mem = self._mem(z)
+        out = self._like(z, g.faces)
+        self._check(self.lib.epc_dct_apply(self.h, C.byref(g), mem, self._ptr(z), alpha, rho,
+                                           self._ptr(out)))
+        return out
+
+    def distance_hessian_apply(self, g, ip, im, b, p):
+        """DistanceEval::hessian_apply (objective.cpp:128-147) at b."""
+        mem = self._mem(ip, im, b, p)
+        out = self._like(p, g.faces)
+        self._check(self.lib.epc_distance_hessian_apply(self.h, C.byref(g), mem, self._ptr(ip),
+                                                        self._ptr(im), self._ptr(b), self._ptr(p),
+                                                        self._ptr(out)))
+        return out
+
+    def is_strictly_feasible(self, g, b):
+        """is_strictly_feasible (objective.cpp:35-37)."""
+        f = C.c_int(0)
+        self._check(self.lib.epc_is_strictly_feasible(self.h, C.byref(g), self._mem(b),
+                                                      self._ptr(b), C.byref(f)))
+        return bool(f.value)
+
     # ---- either side of the solve (image.hpp:62-86) ------------------------------
     def correct_pair(self, g, ip, im, b):
         """correct_pair (image.cpp:226-253) -> (corrected plus, corrected minus)."""
