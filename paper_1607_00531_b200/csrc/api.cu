@@ -356,8 +356,6 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
                    const double* rho_dev, const int* active_dev, double alpha,
                    const epc_admm_config* cfg) {
     const long long total = g.ncol * npairs;
-    const size_t smem = bstep_smem_bytes(g.n1);
-    if (smem > ctx->smem_optin) fail(EPC_ERR_UNSUPPORTED, "column too long for shared memory");
     const HDiv hd = make_hdiv(g.h1);
     // EPC_BSTEP_TAIL (dev aid): per-CTA exit times and per-column durations,
     // recorded by the diagnostic instantiation only
@@ -368,10 +366,23 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
 #else
     const bool diag_forced = false;
 #endif
+    // images in shared memory, or through L1 for long columns: at n1 = 513
+    // (C5) that is 5 resident columns per SM instead of 4 and a 4% faster
+    // b-step; at n1 = 257 (C3) the staged images are 2% faster (measured).
+    // Dev aid EPC_BSTEP_IMG=0/1 forces either; the diagnostic build stages.
+    bool img_global = g.n1 >= 400;
+    if (const char* e = getenv("EPC_BSTEP_IMG")) img_global = atoi(e) != 0;
+    if (diag || diag_forced) img_global = false;
+    const size_t smem = bstep_smem_bytes(g.n1, img_global);
+    if (smem > ctx->smem_optin) fail(EPC_ERR_UNSUPPORTED, "column too long for shared memory");
 
     void (*kern)(BStepParams) =
-        hd.pow2 ? (diag || diag_forced ? k_admm_bstep_t<HPow2, true> : k_admm_bstep_t<HPow2, false>)
-                : (diag || diag_forced ? k_admm_bstep_t<HGen, true> : k_admm_bstep_t<HGen, false>);
+        hd.pow2 ? (diag || diag_forced ? k_admm_bstep_t<HPow2, true, false>
+                                       : (img_global ? k_admm_bstep_t<HPow2, false, true>
+                                                     : k_admm_bstep_t<HPow2, false, false>))
+                : (diag || diag_forced ? k_admm_bstep_t<HGen, true, false>
+                                       : (img_global ? k_admm_bstep_t<HGen, false, true>
+                                                     : k_admm_bstep_t<HGen, false, false>));
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)ctx->smem_optin));
     int per_sm = 0;

@@ -33,7 +33,9 @@ struct BStepParams {
 };
 // DH = HPow2 | HGen (model.cuh); DIAG: phase timing / counters and the
 // chained mode compiled in (diagnostic instantiation, selected by ctx->mode)
-template <class DH, bool DIAG>
+// IMG: I+/I- read from global memory through L1 instead of staged in shared
+// memory (long columns: two fewer vectors per column, more resident columns)
+template <class DH, bool DIAG, bool IMG = false>
 __global__ void k_admm_bstep_t(BStepParams P);
 
 struct QpBatchParams {
@@ -49,7 +51,7 @@ struct QpBatchParams {
     int qcap;
 };
 __global__ void k_qp_batch(QpBatchParams P);
-size_t bstep_smem_bytes(int n1);
+size_t bstep_smem_bytes(int n1, bool img_global = false);
 // Per-warp q-row scratch: qcap rows of n doubles plus CHAIN_PAD before and
 // after (the chain sweeps read the pads).
 __host__ __device__ inline size_t qrows_stride(int qcap, int n) {
