@@ -15,6 +15,8 @@
 // within a few ulps of the sequential sums.
 #include "common.cuh"
 #include "kernels.h"
+
+#include <algorithm>
 #include "model.cuh"
 
 // phi, phi_d1, phi_d2 (objective.cpp:17-33)
@@ -245,6 +247,82 @@ __global__ void __launch_bounds__(128) k_gn_factor(const double* pdiag, const do
         __syncwarp();
     }
 }
+
+// The same factorization with one thread per column: a 256-thread block
+// stages FCPW consecutive columns (one contiguous span) with coalesced loads,
+// then thread c runs column c's pivot chain in shared memory (d over the
+// staged diagonal, l over the staged off-diagonal, each read before it is
+// overwritten) and the span is stored coalesced. Same operations in the same
+// order as TridiagFactor::factorize (operators.cpp:218-246): bitwise.
+constexpr int FCPW = 16;
+__global__ void __launch_bounds__(256) k_gn_factor_cols(const double* pdiag, const double* off,
+                                                       double* fd, double* fl, int n1,
+                                                       long long ncol, int rs, int* col_err) {
+    extern __shared__ __align__(16) double fsm[];
+    double* X = fsm;            // diagonal -> pivots d
+    double* Y = fsm + FCPW * rs;  // off-diagonal -> multipliers l
+    const int tid = threadIdx.x;
+    const unsigned un1 = (unsigned)n1;
+    const long long ngroups = (ncol + FCPW - 1) / FCPW;
+    for (long long gi = blockIdx.x; gi < ngroups; gi += gridDim.x) {
+        const long long c0 = gi * FCPW;
+        const int nc = (int)(ncol - c0 < FCPW ? ncol - c0 : FCPW);
+        const size_t base = (size_t)c0 * n1;
+        const int ne = nc * n1;
+#pragma unroll 4
+        for (int e = tid; e < ne; e += blockDim.x) {
+            const int cc = (int)((unsigned)e / un1), i = e - cc * n1;
+            X[cc * rs + i] = pdiag[base + e];
+            Y[cc * rs + i] = off[base + e];
+        }
+        __syncthreads();
+        if (tid < nc) {
+            double* x = X + tid * rs;
+            double* y = Y + tid * rs;
+            int bad = 0;
+            double prev = x[0];
+            if (!(prev > 0.0)) {
+                bad = 1;
+            } else {
+                for (int i = 1; i < n1; ++i) {
+                    const double oo = y[i - 1];
+                    const double li = oo / prev;
+                    y[i - 1] = li;
+                    const double piv = x[i] - li * oo;
+                    if (!(piv > 0.0)) {
+                        bad = 1;
+                        break;
+                    }
+                    x[i] = piv;
+                    prev = piv;
+                }
+                y[n1 - 1] = 0.0;
+            }
+            col_err[c0 + tid] = bad;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int e = tid; e < ne; e += blockDim.x) {
+            const int cc = (int)((unsigned)e / un1), i = e - cc * n1;
+            fd[base + e] = X[cc * rs + i];
+            fl[base + e] = Y[cc * rs + i];
+        }
+        __syncthreads();
+    }
+}
+
+void launch_gn_factor_cols(epc_context* ctx, const double* pdiag, const double* off, double* fd,
+                           double* fl, int n1, long long ncol, int* col_err) {
+    const int rs = n1 | 1;
+    const size_t smem = (size_t)2 * FCPW * rs * sizeof(double);
+    cudaFuncSetAttribute(k_gn_factor_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const long long groups = (ncol + FCPW - 1) / FCPW;
+    const int blocks = (int)std::max<long long>(1, std::min<long long>(groups, (long long)ctx->num_sms * 8));
+    EPC_LAUNCH(ctx, "gn_factor", k_gn_factor_cols, blocks, 256, smem, pdiag, off, fd, fl, n1, ncol, rs,
+               col_err);
+}
+
+size_t gn_factor_cols_smem(int n1) { return (size_t)2 * FCPW * (n1 | 1) * sizeof(double); }
 
 // GnHessian::apply (objective.cpp:302-331) fused with the PCG direction
 // update p = z + beta p (gn_pcg.cpp:128); beta_mode: 0 -> p = z (first

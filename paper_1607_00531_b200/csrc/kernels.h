@@ -295,3 +295,8 @@ void launch_distance_hv(epc_context* ctx, const double* jlo, const double* jhi, 
                         int m1, long long nface, double V, double* out);
 int launch_d1_absmax(epc_context* ctx, const double* b, int m1, long long ncell, double ih,
                      double* part);
+
+// TridiagFactor::factorize with one thread per column over staged column groups (gn.cu)
+void launch_gn_factor_cols(epc_context* ctx, const double* pdiag, const double* off, double* fd,
+                           double* fl, int n1, long long ncol, int* col_err);
+size_t gn_factor_cols_smem(int n1);
