@@ -655,18 +655,26 @@ def main():
     b_ach = alg.get(bname, 0) / b_per / 1e9
     # DRAM traffic of one b-step launch from the committed ncu --set full
     # capture summary (scripts/summarize_ncu.py), bytes per launch
-    traffic, traffic_src = None, None
+    traffic, traffic_src, pipe = None, None, None
     try:
         cap = json.load(open(os.path.join(ROOT, "profiles", NCU_BSTEP_SUMMARY)))
         mb = float(cap["dram__bytes_read.sum"][0]) + float(cap["dram__bytes_write.sum"][0])
         if cap["dram__bytes_read.sum"][1] == "Mbyte":
             traffic, traffic_src = mb * 1e6, "profiles/" + NCU_BSTEP_SUMMARY
+        # what does bound it: issue and fp64-pipe activity and the stall mix
+        stalls = cap.get("stall_mix_pct", {})
+        pipe = {"issue_active_frac": float(cap["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]) / 100,
+                "fp64_pipe_active_frac":
+                    float(cap["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"][0]) / 100,
+                "top_stall": max(stalls.items(), key=lambda kv: kv[1])[0] if stalls else None,
+                "source": "profiles/" + NCU_BSTEP_SUMMARY}
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": bname, "achieved": b_ach, "peak": hbm_peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": b_ach / hbm_peak,
                 "traffic": traffic, "traffic_source": traffic_src, "share_of_step": bms / sum(v[0] for v in prof.values()),
                 "note": "b-step is fp64-latency bound (serial SQP/QP chains), not HBM bound",
+                "bstep_pipes": pipe,
                 "kernels": kernels}
 
     cpu = None
