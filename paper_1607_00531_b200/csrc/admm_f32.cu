@@ -494,8 +494,17 @@ __global__ void __launch_bounds__(32, 16) k_bstep_f32(BStepF32Params P) {
             if (lane == 0) P.col_err[col] = err;
             continue;
         }
-        // clamp_column_diffs (admm.cpp:99-110), lane 0, fp32 nextafter
-        if (lane == 0) {
+        // clamp_column_diffs (admm.cpp:99-110), lane 0, fp32 nextafter; skipped
+        // when it is the identity (every step's own comparisons hold with a
+        // zero shift; -0.0 + 0.0 would turn into +0.0)
+        int ident = 1;
+        for (int i = lane; i + 1 < n1; i += 32) {
+            const float xi = x[i], nx = x[i + 1], t = (nx - xi) / h;
+            if ((nx == 0.0f && signbit(nx)) || nx < xi - h || xi + h < nx || t > 1.0f || t < -1.0f)
+                ident = 0;
+        }
+        const bool identity = __all_sync(FULL_MASK, ident) != 0;
+        if (lane == 0 && !identity) {
             float shift = 0.0f;
             for (int i = 0; i + 1 < n1; ++i) {
                 const float nx = x[i + 1] + shift;
