@@ -20,15 +20,20 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace {
-constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
+constexpr int BN = 64, BK = 16, NT = 256;
 }
 
-template <int PRO, int EPI>
+// RM rows per thread: BM = 16 RM output rows per CTA (RM = 4: 64; RM = 6: 96,
+// which tiles the axis-3 transforms of m3 = 96 without a half-empty tile)
+template <int PRO, int EPI, int RM>
 // The dual epilogue needs more registers than the plain ones; capping it to
 // three resident CTAs per SM (<= 85 registers) is faster than two with more
 // registers (measured), the other variants fit three CTAs unforced.
 __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmParams p) {
+    constexpr int BM = 16 * RM;
     __shared__ double As[BK][BM + 1];  // +1: the transposing store is conflict-free
     __shared__ double Bs[BK][BN];
     __shared__ double red[(NT / 32) * 6];
@@ -48,16 +53,16 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
     // this thread's A-load element
     const int am = tid >> 4 /*0..15*/, ak = tid & 15;
 
-    double acc[4][4];
+    double acc[RM][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < RM; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
 
-    double ra[4], rb[4];
+    double ra[RM], rb[4];
     auto load_tile = [&](int k0) {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < RM; ++t) {
             const int m = am + 16 * t, k = k0 + ak;
             ra[t] = (row0 + m < p.M && k < p.K) ? __ldg(p.A + (size_t)(row0 + m) * p.K + k) : 0.0;
         }
@@ -78,7 +83,7 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
     for (int k0 = 0; k0 < p.K; k0 += BK) {
         __syncthreads();
 #pragma unroll
-        for (int t = 0; t < 4; ++t) As[ak][am + 16 * t] = ra[t];
+        for (int t = 0; t < RM; ++t) As[ak][am + 16 * t] = ra[t];
 #pragma unroll
         for (int t = 0; t < 4; ++t) Bs[lk + 4 * t][ln] = rb[t];
         __syncthreads();
@@ -87,25 +92,25 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
         if (kend == BK) {
 #pragma unroll
             for (int kk = 0; kk < BK; ++kk) {
-                double a[4], b[4];
+                double a[RM], b[4];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
+                for (int r = 0; r < RM; ++r) a[r] = As[kk][ty + 16 * r];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
 #pragma unroll
-                for (int r = 0; r < 4; ++r)
+                for (int r = 0; r < RM; ++r)
 #pragma unroll
                     for (int c = 0; c < 4; ++c) acc[r][c] = acc[r][c] + a[r] * b[c];
             }
         } else {
             for (int kk = 0; kk < kend; ++kk) {
-                double a[4], b[4];
+                double a[RM], b[4];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
+                for (int r = 0; r < RM; ++r) a[r] = As[kk][ty + 16 * r];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
 #pragma unroll
-                for (int r = 0; r < 4; ++r)
+                for (int r = 0; r < RM; ++r)
 #pragma unroll
                     for (int c = 0; c < 4; ++c) acc[r][c] = acc[r][c] + a[r] * b[c];
             }
@@ -120,7 +125,7 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
         if (col >= p.N) continue;
         const long long cmap = (col / p.cdiv) * p.cstride + (col % p.cdiv);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < RM; ++r) {
             const int row = row0 + ty + 16 * r;
             if (row >= p.M) continue;
             const long long f = zoff + (long long)row * p.kstride + cmap;
@@ -172,20 +177,35 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
     }
 }
 
-void launch_dct_gemm(epc_context* ctx, const char* name, const GemmParams& p, int pro, int epi,
-                     int nz, int* nblocks_out) {
+template <int RM>
+void launch_dct_gemm_rm(epc_context* ctx, const char* name, const GemmParams& p, int pro, int epi,
+                        int nz, int* nblocks_out) {
+    constexpr int BM = 16 * RM;
     dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + BM - 1) / BM), (unsigned)nz);
     if (nblocks_out) *nblocks_out = (int)(grid.x * grid.y);
     if (pro == PRO_RHS && epi == EPI_STORE)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_STORE>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_STORE, RM>), grid, NT, 0, p);
     else if (pro == PRO_RHS && epi == EPI_DIVIDE)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_DIVIDE>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_DIVIDE, RM>), grid, NT, 0, p);
     else if (pro == PRO_PLAIN && epi == EPI_DIVIDE)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DIVIDE>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DIVIDE, RM>), grid, NT, 0, p);
     else if (pro == PRO_PLAIN && epi == EPI_DUAL)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DUAL>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DUAL, RM>), grid, NT, 0, p);
     else
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_STORE>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_STORE, RM>), grid, NT, 0, p);
+}
+
+// 96-row tiles for the plain-store transforms when M is a multiple of 96
+// (the inverse axis-3 transform at m3 = 96: 0.130 -> 0.111 ms at C3), else
+// 64: the divide and dual epilogues are slower with 96 (measured).
+// EPC_GEMM_RM=4 forces 64-row tiles (dev aid).
+void launch_dct_gemm(epc_context* ctx, const char* name, const GemmParams& p, int pro, int epi,
+                     int nz, int* nblocks_out) {
+    static const bool force64 = getenv("EPC_GEMM_RM") && atoi(getenv("EPC_GEMM_RM")) == 4;
+    if (!force64 && epi == EPI_STORE && p.M % 96 == 0)
+        launch_dct_gemm_rm<6>(ctx, name, p, pro, epi, nz, nblocks_out);
+    else
+        launch_dct_gemm_rm<4>(ctx, name, p, pro, epi, nz, nblocks_out);
 }
 
 // g_value parts (admm.cpp:275-285): sum over faces of (D2 z)^2 and (D3 z)^2,
