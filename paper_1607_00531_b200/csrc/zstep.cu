@@ -177,35 +177,39 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
     }
 }
 
-template <int RM>
-void launch_dct_gemm_rm(epc_context* ctx, const char* name, const GemmParams& p, int pro, int epi,
+void launch_dct_gemm_64(epc_context* ctx, const char* name, const GemmParams& p, int pro, int epi,
                         int nz, int* nblocks_out) {
-    constexpr int BM = 16 * RM;
+    constexpr int BM = 64;
     dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + BM - 1) / BM), (unsigned)nz);
     if (nblocks_out) *nblocks_out = (int)(grid.x * grid.y);
     if (pro == PRO_RHS && epi == EPI_STORE)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_STORE, RM>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_STORE, 4>), grid, NT, 0, p);
     else if (pro == PRO_RHS && epi == EPI_DIVIDE)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_DIVIDE, RM>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_DIVIDE, 4>), grid, NT, 0, p);
     else if (pro == PRO_PLAIN && epi == EPI_DIVIDE)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DIVIDE, RM>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DIVIDE, 4>), grid, NT, 0, p);
     else if (pro == PRO_PLAIN && epi == EPI_DUAL)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DUAL, RM>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DUAL, 4>), grid, NT, 0, p);
     else
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_STORE, RM>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_STORE, 4>), grid, NT, 0, p);
 }
 
 // 96-row tiles for the plain-store transforms when M is a multiple of 96
 // (the inverse axis-3 transform at m3 = 96: 0.130 -> 0.111 ms at C3), else
-// 64: the divide and dual epilogues are slower with 96 (measured).
-// EPC_GEMM_RM=4 forces 64-row tiles (dev aid).
+// 64: the divide and dual epilogues are slower with 96 and 128-row tiles are
+// slower for the axis-2 transforms (measured). EPC_GEMM_RM=4 forces 64-row
+// tiles (dev aid).
 void launch_dct_gemm(epc_context* ctx, const char* name, const GemmParams& p, int pro, int epi,
                      int nz, int* nblocks_out) {
     static const bool force64 = getenv("EPC_GEMM_RM") && atoi(getenv("EPC_GEMM_RM")) == 4;
-    if (!force64 && epi == EPI_STORE && p.M % 96 == 0)
-        launch_dct_gemm_rm<6>(ctx, name, p, pro, epi, nz, nblocks_out);
-    else
-        launch_dct_gemm_rm<4>(ctx, name, p, pro, epi, nz, nblocks_out);
+    if (!force64 && pro == PRO_PLAIN && epi == EPI_STORE && p.M % 96 == 0) {
+        constexpr int BM = 96;
+        dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + BM - 1) / BM), (unsigned)nz);
+        if (nblocks_out) *nblocks_out = (int)(grid.x * grid.y);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_STORE, 6>), grid, NT, 0, p);
+    } else {
+        launch_dct_gemm_64(ctx, name, p, pro, epi, nz, nblocks_out);
+    }
 }
 
 // g_value parts (admm.cpp:275-285): sum over faces of (D2 z)^2 and (D3 z)^2,
