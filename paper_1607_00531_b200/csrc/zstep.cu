@@ -23,7 +23,11 @@
 #include <cstdlib>
 
 namespace {
-constexpr int BN = 64, BK = 16, NT = 256;
+#ifndef EPC_GEMM_BK
+#define EPC_GEMM_BK 16  // k-slab depth; 32 measured slower for three of the four transforms
+#endif
+constexpr int BN = 64, BK = EPC_GEMM_BK, NT = 256;
+constexpr int AR = NT / BK;  // A-tile rows loaded per pass (a thread per k column)
 }
 
 // RM rows per thread: BM = 16 RM output rows per CTA (RM = 4: 64; RM = 6: 96,
@@ -44,14 +48,15 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
     const long long zoff = (long long)pair * p.zstride;
 
     // this thread's B-load column (fixed across the K loop)
-    const int ln = tid & 63, lk = tid >> 6;  // 4 rows lk, lk+4, lk+8, lk+12
+    const int ln = tid & 63, lk = tid >> 6;  // BK/4 rows lk, lk+4, ...
     const long long lcol = col0 + ln;
     const bool lcol_ok = lcol < p.N;
     const long long lmap = lcol_ok ? (lcol / p.cdiv) * p.cstride + (lcol % p.cdiv) : 0;
     double wrhs = 0.0;
     if (PRO == PRO_RHS) wrhs = p.rho[pair] * p.V;
     // this thread's A-load element
-    const int am = tid >> 4 /*0..15*/, ak = tid & 15;
+    const int am = tid / BK, ak = tid % BK;
+    constexpr int NA = BM / AR, NB = BK / 4;  // A and B elements per thread per slab
 
     double acc[RM][4];
 #pragma unroll
@@ -59,15 +64,15 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
 
-    double ra[RM], rb[4];
+    double ra[NA], rb[NB];
     auto load_tile = [&](int k0) {
 #pragma unroll
-        for (int t = 0; t < RM; ++t) {
-            const int m = am + 16 * t, k = k0 + ak;
+        for (int t = 0; t < NA; ++t) {
+            const int m = am + AR * t, k = k0 + ak;
             ra[t] = (row0 + m < p.M && k < p.K) ? __ldg(p.A + (size_t)(row0 + m) * p.K + k) : 0.0;
         }
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < NB; ++t) {
             const int k = k0 + lk + 4 * t;
             double v = 0.0;
             if (lcol_ok && k < p.K) {
@@ -83,9 +88,9 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
     for (int k0 = 0; k0 < p.K; k0 += BK) {
         __syncthreads();
 #pragma unroll
-        for (int t = 0; t < RM; ++t) As[ak][am + 16 * t] = ra[t];
+        for (int t = 0; t < NA; ++t) As[ak][am + AR * t] = ra[t];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) Bs[lk + 4 * t][ln] = rb[t];
+        for (int t = 0; t < NB; ++t) Bs[lk + 4 * t][ln] = rb[t];
         __syncthreads();
         if (k0 + BK < p.K) load_tile(k0 + BK);
         const int kend = min(BK, p.K - k0);
