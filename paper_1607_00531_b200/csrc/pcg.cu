@@ -572,7 +572,10 @@ __device__ double block_fixed_sum(const double* part, int n, int stride, int off
 }
 
 template <int CPW>
-__global__ void __launch_bounds__(PCG_NT) k_pcg_loop(PcgLoopArgs L, PcgState* S) {
+#ifndef EPC_PCG_LOOP_MINB
+#define EPC_PCG_LOOP_MINB 4  // 64 registers: 4 resident blocks per SM (C2 GN solve 29.4 -> 23.0 ms; 5 spills)
+#endif
+__global__ void __launch_bounds__(PCG_NT, EPC_PCG_LOOP_MINB) k_pcg_loop(PcgLoopArgs L, PcgState* S) {
     extern __shared__ __align__(16) double usm[];
     __shared__ double sh[8];
     double* const X = usm;
