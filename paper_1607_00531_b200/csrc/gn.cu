@@ -40,7 +40,10 @@ __device__ __forceinline__ double phi_d2(double x) {
 // cells: residual, Jacobian, penalty terms; partial sums per block:
 // {sum r^2, sum (D1 b)^2, sum phi(D1 b), max |D1 b|}
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_gn_cells(GnCellArgs A) {
+#ifndef EPC_GN_CELLS_MINB
+#define EPC_GN_CELLS_MINB 4  // 64 registers, 4 blocks per SM: 41 -> 30 us at C2 (measured)
+#endif
+__global__ void __launch_bounds__(256, EPC_GN_CELLS_MINB) k_gn_cells(GnCellArgs A) {
     __shared__ double sh[16];
     const ColGeom geo{A.m1, A.o1, A.dh};
     const double ih = 1.0 / A.dh.h;
