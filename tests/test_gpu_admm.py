@@ -164,6 +164,30 @@ def test_admm_c1_bitwise(ctx, oracle):
         assert a["lagrangian"] == pytest.approx(r["lagrangian"], rel=1e-9)
 
 
+@pytest.mark.slow
+def test_admm_c3_bench_config_bitwise_vs_reference(ctx):
+    """The bench's own workload (BASELINE configs[2], 256x256x96) against the
+    compiled reference library itself (oracle/_ref, all host threads) for the
+    first 3 ADMM iterations: b, z, u, rho and every row bitwise."""
+    import os
+    from oracle import ffi
+    if not ffi.available("ref"):
+        pytest.skip("reference library not available")
+    ref = ffi.load("ref")
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    d = synth.make_config("C3")
+    cfg = abi.AdmmConfig(max_iter=3, threads=threads, **EXACT)
+    r = ref.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
+    o = ctx.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
+    for k in ("b", "z", "u"):
+        assert np.array_equal(o[k], r[k]), k
+    assert o["rho"] == r["rho"] and o["stop"] == r["stop"]
+    for a, b in zip(o["rows"], r["rows"]):
+        assert a["rho"] == b["rho"] and a["kkt_violation"] == b["kkt_violation"]
+        assert a["lagrangian"] == pytest.approx(b["lagrangian"], rel=1e-12)
+
+
 @pytest.mark.parametrize("scale", [1.0, 400.0])
 def test_bstep_modes_bitwise(ctx, oracle, scale):
     """The certified-enclosure b-step (default), the diagnostic instantiation
