@@ -656,7 +656,7 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
                                     batch ? act_dev : nullptr, p->alpha, cfg);
             CK(cudaEventRecord(eb1, ctx->stream));
             const long long total = g.ncol * npairs;
-            EPC_LAUNCH(ctx, "reduce_columns", k_reduce_columns, npairs, 256, 0, br.col_i,
+            EPC_LAUNCH(ctx, "reduce_columns", k_reduce_columns, npairs, 1024, 0, br.col_i,
                        br.col_i + total, br.col_i + 2 * total, br.col_i + 3 * total, br.col_d,
                        br.col_d + total, br.col_d + 2 * total, g.ncol,
                        batch ? act_dev : nullptr, scal_d, scal_i);
@@ -1041,7 +1041,7 @@ int epc_b_update(epc_context* ctx, const epc_grid* gg, int mem, const double* ip
         double* sd = slot_t<double>(ctx, S_SCAL, 4);
         long long* si = slot_t<long long>(ctx, S_TMP1, 6);
         const long long total = g.ncol;
-        EPC_LAUNCH(ctx, "reduce_columns", k_reduce_columns, 1, 256, 0, br.col_i, br.col_i + total,
+        EPC_LAUNCH(ctx, "reduce_columns", k_reduce_columns, 1, 1024, 0, br.col_i, br.col_i + total,
                    br.col_i + 2 * total, br.col_i + 3 * total, br.col_d, br.col_d + total,
                    br.col_d + 2 * total, g.ncol, nullptr, sd, si);
         double hd[4];

@@ -274,14 +274,14 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const double* in, int n
 // Per-pair reduction of the b-step's per-column outputs. out_d[pair*4]:
 // {kkt max, sum r^2, sum (D1 b)^2, 0}; out_i[pair*6]: {first failing column or
 // -1, its error code, sqp total, qp total, max active, 0}.
-__global__ void __launch_bounds__(256) k_reduce_columns(const int* col_err, const int* col_sqp,
+__global__ void __launch_bounds__(1024) k_reduce_columns(const int* col_err, const int* col_sqp,
                                                        const int* col_qp, const int* col_maxact,
                                                        const double* col_kkt, const double* col_fr,
                                                        const double* col_fd, long long ncol,
                                                        const int* active, double* out_d,
                                                        long long* out_i) {
-    __shared__ double sh[8];
-    __shared__ long long shi[8][4];
+    __shared__ double sh[32];
+    __shared__ long long shi[32][4];
     const int pair = blockIdx.x;
     if (active && !active[pair]) return;
     const long long base = (long long)pair * ncol;
