@@ -68,7 +68,7 @@ def parse():
 
 # fp64 DADD/DMUL issue rate measured on this pool (profiles/r01_ubench_fp64_tput.log)
 FP64_PEAK_TOPS = 18.3
-NCU_BSTEP_SUMMARY = "r01i_bstep_ncu.json"  # C3 b-step, one launch, ncu --set full
+NCU_BSTEP_SUMMARY = "r01l_bstep_ncu.json"  # C3 b-step, one launch, ncu --set full
 DEFAULT_ITERS = {"C1": 50, "C2": 50, "C3": 100, "C4": 50, "C5": 50}
 
 
@@ -131,7 +131,13 @@ def dist_setup(n):
     local = int(os.environ.get("LOCAL_RANK", rank))
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29511")
-    dist.init_process_group("nccl", rank=rank, world_size=world)
+    import torch
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group("nccl", rank=rank, world_size=world)
     return rank, world, local, dist
 
 
@@ -269,10 +275,13 @@ def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
             npcg += r if isinstance(r, int) else sum(x["pcg_iters"] for x in r["rows"])
         return tot, launches, npcg
 
-    for _ in range(a.warmup):
+    # a GN solve is ~25 ms with 10 host round trips: time at least 10 solves
+    # so host scheduling jitter averages out
+    gk = max(a.steps, 10)
+    for _ in range(max(a.warmup, 3)):
         solve_device()
-    t_dev, launches, npcg = timed(solve_device, a.steps)
-    t_e2e, _, npcg_h = timed(solve_host, a.steps)
+    t_dev, launches, npcg = timed(solve_device, gk)
+    t_e2e, _, npcg_h = timed(solve_host, gk)
     from paper_1607_00531_b200 import shard
     t_dev = shard.max_over_ranks(t_dev, dist, dev)
     t_e2e = shard.max_over_ranks(t_e2e, dist, dev)
@@ -280,7 +289,7 @@ def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
     # per-kernel times of one profiled solve; algorithmic bytes per face per
     # launch: pcg_hvp reads z, p_old, diag, off and writes p, q
     # (48 B); pcg_update reads d, r, p, q, fd, fl and writes d, r, z (72 B).
-    # The profiled solve is one solve; npcg counts a.steps solves.
+    # The profiled solve is one solve; npcg counts gk solves.
     ctx.profile(True)
     ctx.profile_reset()
     solve_device()
@@ -289,7 +298,7 @@ def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
     per_face = {"pcg_update": 72, "pcg_hvp": 48}
     # the persistent loop kernel runs both phases (120 B/face per PCG
     # iteration) for all iterations of one PCG solve per launch
-    loop_iters = npcg / a.steps / max(1, prof.get("pcg_loop", (0, 0))[1])
+    loop_iters = npcg / gk / max(1, prof.get("pcg_loop", (0, 0))[1])
     kernels = []
     for name, (ms, n) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
         if not n:
@@ -318,7 +327,7 @@ def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
                         "C2 vectors are 8.5 MB, so launch ramp and grid barriers weigh"}
     out = {"metric": f"voxel-iterations/s (GN-PCG, {'x'.join(map(str, g.dims()))}, fp64)",
            "value": g.faces * npcg / t_dev * world, "unit": GN_UNIT,
-           "time_to_solution_s": t_dev / a.steps, "pcg_iterations_per_solve": npcg // a.steps,
+           "steps": gk, "time_to_solution_s": t_dev / gk, "pcg_iterations_per_solve": npcg // gk,
            "workload": f"GN-PCG {a.gn_config} block-Jacobi, 10 GN steps x <=50 PCG, eta 1e-2",
            "e2e": {"value": g.faces * npcg_h / t_e2e * world, "unit": GN_UNIT,
                    "h2d_bytes_per_step": (2 * g.cells + g.faces) * 8,
