@@ -100,7 +100,7 @@ __device__ bool factor_f(const float* __restrict__ gd, const float* __restrict__
     for (int i = 1; i < n; ++i) {
         const float o = go[i - 1];
         const float l = o * r;
-        const float d = gd[i] - l * o;
+        const float d = __fmaf_rn(-l, o, gd[i]);
         r = __frcp_rn(d);
         fl[i - 1] = l;
         rd[i] = r;
@@ -116,16 +116,125 @@ __device__ void solve_f(float* __restrict__ x, const float* __restrict__ rd,
     float prev = x[0];
 #pragma unroll 8
     for (int i = 1; i < n; ++i) {
-        prev = x[i] - fl[i - 1] * prev;
+        prev = __fmaf_rn(-fl[i - 1], prev, x[i]);
         x[i] = prev;
     }
     float nxt = x[n - 1] * rd[n - 1];
     x[n - 1] = nxt;
 #pragma unroll 8
     for (int i = n - 2; i >= 0; --i) {
-        nxt = x[i] * rd[i] - fl[i] * nxt;
+        nxt = __fmaf_rn(-fl[i], nxt, x[i] * rd[i]);
         x[i] = nxt;
     }
+}
+
+// The same factor and w solve as 32-lane segmented chains with agreement
+// rounds (bstep.cu, seg_sweep): each lane runs S steps from a start value
+// (exact on lane 0, a guess elsewhere) until every lane's start equals its
+// predecessor's end bitwise; the stored values are then the one-thread
+// loops' above. Falls back to them after FSEG_ROUNDS rounds.
+constexpr int FSEG_ROUNDS = 8;
+__device__ __forceinline__ int fseg_len(int steps) { return ((steps + 31) >> 5) | 1; }
+__device__ __forceinline__ bool fseg_agree(float end, int cnt, float& st) {
+    const int lane = threadIdx.x & 31;
+    const float pe = __shfl_up_sync(FULL_MASK, end, 1);
+    const bool ok = lane == 0 || cnt == 0 || __float_as_int(pe) == __float_as_int(st);
+    if (__all_sync(FULL_MASK, ok)) return true;
+    if (lane > 0) st = pe;
+    return false;
+}
+
+// factor_f in segments: 1 ok, 0 nonpositive pivot, -1 no agreement
+template <int S>
+__device__ __forceinline__ int factor_f_seg(const float* __restrict__ gd,
+                                            const float* __restrict__ go, float* __restrict__ rd,
+                                            float* __restrict__ fl, int n) {
+    const int lane = threadIdx.x & 31;
+    const int i0 = 1 + lane * S;
+    const int cnt = max(0, min(S, n - i0));
+    if (lane == 0) {
+        rd[0] = __frcp_rn(gd[0]);
+        fl[n - 1] = 0.0f;
+    }
+    float st = gd[min(i0, n) - 1];
+    for (int round = 0; round < FSEG_ROUNDS; ++round) {
+        float prev = st, end = st;
+        bool ok = lane != 0 || gd[0] > 0.0f;
+        float r = __frcp_rn(prev);
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            const int i = min(i0 + j, n - 1);
+            const float o = go[i - 1];
+            const float l = o * r;
+            const float d = __fmaf_rn(-l, o, gd[i]);
+            r = __frcp_rn(d);
+            if (j < cnt) {
+                fl[i - 1] = l;
+                rd[i] = r;
+                ok = ok && d > 0.0f;
+            }
+            if (j == cnt - 1) end = d;
+            prev = d;
+        }
+        if (fseg_agree(end, cnt, st)) return __all_sync(FULL_MASK, ok) ? 1 : 0;
+    }
+    return -1;
+}
+
+// solve_f's sweeps, out of place: forward src -> dst, or backward with the
+// pivot reciprocals (dst[e] = src[e] rd[e] - fl[e] dst[e+1])
+template <int S, bool BWD>
+__device__ __forceinline__ bool fseg_sweep(const float* __restrict__ src, float* __restrict__ dst,
+                                           const float* __restrict__ rd,
+                                           const float* __restrict__ fl, int n) {
+    const int lane = threadIdx.x & 31;
+    const int r0 = 1 + lane * S;
+    const int cnt = max(0, min(S, n - r0));
+    if (lane == 0) dst[BWD ? n - 1 : 0] = BWD ? src[n - 1] * rd[n - 1] : src[0];
+    const int e0 = BWD ? n - min(r0, n) : min(r0, n) - 1;
+    float st = BWD ? src[e0] * rd[e0] : src[e0];
+    for (int round = 0; round < FSEG_ROUNDS; ++round) {
+        float p = st, end = st;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            const int r = min(r0 + j, n - 1);
+            const int e = BWD ? n - 1 - r : r;
+            p = BWD ? __fmaf_rn(-fl[e], p, src[e] * rd[e]) : __fmaf_rn(-fl[e - 1], p, src[e]);
+            if (j < cnt) dst[e] = p;
+            if (j == cnt - 1) end = p;
+        }
+        if (fseg_agree(end, cnt, st)) return true;
+    }
+    return false;
+}
+
+// w = G^{-1} w through the scratch t (all lanes)
+template <int S>
+__device__ __forceinline__ void solve_w_f_seg(float* __restrict__ w, float* __restrict__ t,
+                                              const float* __restrict__ rd,
+                                              const float* __restrict__ fl, int n) {
+    const int lane = threadIdx.x & 31;
+    if (!fseg_sweep<S, false>(w, t, rd, fl, n)) {  // w untouched: the one-thread solve
+        __syncwarp();
+        if (lane == 0) solve_f(w, rd, fl, n);
+        __syncwarp();
+        return;
+    }
+    __syncwarp();
+    if (fseg_sweep<S, true>(t, w, rd, fl, n)) {
+        __syncwarp();
+        return;
+    }
+    __syncwarp();
+    if (lane == 0) {  // solve_f's backward loop from the forward result in t
+        float nxt = t[n - 1] * rd[n - 1];
+        w[n - 1] = nxt;
+        for (int i = n - 2; i >= 0; --i) {
+            nxt = __fmaf_rn(-fl[i], nxt, t[i] * rd[i]);
+            w[i] = nxt;
+        }
+    }
+    __syncwarp();
 }
 
 enum { FQ_OK = 0, FQ_PIVOT = 1, FQ_INFEASIBLE = 2, FQ_SCHUR = 3, FQ_CYCLE = 4 };
@@ -138,7 +247,14 @@ __device__ int qp_f32(const BStepF32Params& P, const ColF& s, int n, float* qscr
     float *gd = s.a(F_GD), *go = s.a(F_GO), *cq = s.a(F_CQ), *x = s.a(F_QX), *w = s.a(F_W);
     float *p = s.a(F_P), *fd = s.a(F_FD), *fl = s.a(F_FL), *lam = s.a(F_LAM);
     int bad = 0;
-    if (lane == 0) bad = !factor_f(gd, go, fd, fl, n);
+    {
+        const int S = fseg_len(n - 1);
+        const int seg = S <= 9 ? factor_f_seg<9>(gd, go, fd, fl, n)
+                                : (S <= 17 ? factor_f_seg<17>(gd, go, fd, fl, n) : -1);
+        __syncwarp();
+        if (seg >= 0) bad = !seg;
+        else if (lane == 0) bad = !factor_f(gd, go, fd, fl, n);
+    }
     if (__shfl_sync(FULL_MASK, bad, 0)) return FQ_PIVOT;
     int infeas = 0;
     for (int i = lane; i < ncell; i += 32) {
@@ -175,7 +291,14 @@ __device__ int qp_f32(const BStepF32Params& P, const ColF& s, int n, float* qscr
         }
         __syncwarp();
         // lane 0: w = G^-1 g; lanes: q rows G^-1 a_r (global scratch)
-        if (lane == 0) solve_f(w, fd, fl, n);
+        // w alone (no active rows): segmented over all lanes, p as scratch
+        const int S = fseg_len(n - 1);
+        if (na == 0 && S <= 17) {
+            if (S <= 9) solve_w_f_seg<9>(w, p, fd, fl, n);
+            else solve_w_f_seg<17>(w, p, fd, fl, n);
+        } else if (lane == 0) {
+            solve_f(w, fd, fl, n);
+        }
         for (int r = lane; r < na; r += 32) {
             float* q = qscr + (size_t)r * n;
             const int ir = s.act[r];
