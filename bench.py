@@ -68,7 +68,7 @@ def parse():
 
 # fp64 DADD/DMUL issue rate measured on this pool (profiles/r01_ubench_fp64_tput.log)
 FP64_PEAK_TOPS = 18.3
-NCU_BSTEP_SUMMARY = "r01l_bstep_ncu.json"  # C3 b-step, one launch, ncu --set full
+NCU_BSTEP_SUMMARY = "r01o_bstep_ncu.json"  # C3 b-step, one launch, ncu --set full
 DEFAULT_ITERS = {"C1": 50, "C2": 50, "C3": 100, "C4": 50, "C5": 50}
 
 
