@@ -216,3 +216,24 @@ def test_bstep_modes_bitwise(ctx, oracle, scale):
     hist = sum(d[k] for k in ("acc0", "acc1", "acc2_3", "acc4_7", "acc8_15", "acc16_31",
                               "acc32_39", "fail"))
     assert hist == d["ls_searches"]
+
+
+@pytest.mark.parametrize("alpha,rho", [(1e4, 1e-2), (50.0, 100.0), (1e-3, 1e6), (2e5, 1.0)])
+def test_b_update_segmented_chains_bitwise(ctx, oracle, alpha, rho):
+    """The LDL^T chain and the sweeps run as 32-lane segments with agreement
+    rounds (csrc/bstep.cu, seg_factor / seg_sweep). A large alpha / rho ratio
+    makes G nearly a Laplacian, whose recurrences barely contract, so the
+    segments need many rounds or fall back to the one-thread chains; a small
+    one makes them agree at once. Every case must match the oracle bitwise,
+    at n1 = 257 (9-step segments), n1 = 301 (too long for the 9-step segments of the staged-image kernel:
+    one-thread chains) and n1 = 513 (long-column kernel, 17-step segments)."""
+    for m in ((256, 4, 3), (300, 3, 2), (512, 3, 2)):
+        g, ip, im = small_pair(m=m, seed=11)
+        st = state_after(oracle, g, ip, im, 3)
+        params = abi.ObjectiveParams(alpha=alpha)
+        ref = oracle.b_update(g, ip, im, st["b"], st["z"], st["u"], rho, params=params)
+        assert ref["rc"] == 0, ref
+        out = ctx.b_update(g, ip, im, st["b"], st["z"], st["u"], rho, params=params)
+        assert np.array_equal(out["b"], ref["b"]), (m, np.abs(out["b"] - ref["b"]).max())
+        assert out["sqp_iters"] == ref["sqp_iters"] and out["qp_iters"] == ref["qp_iters"]
+        assert out["kkt_violation"] == ref["kkt_violation"]
