@@ -154,9 +154,18 @@ enum {
     EPC_MODE_BSTEP_TIMING = 1, /* accumulate b-step phase cycles and counters (diagnostic) */
     /* decide every b-step SQP / line-search test on the reference's sequential
      * sums instead of certified enclosures (diagnostic; identical results) */
-    EPC_MODE_BSTEP_CHAINED = 1 << 13
+    EPC_MODE_BSTEP_CHAINED = 1 << 13,
+    /* take every ADMM stop / rho decision on the reference's sequential sums
+     * (k_seq_sums) instead of certifying it from the tree sums (diagnostic;
+     * identical decisions, and the rows' residuals become bitwise the
+     * reference's) */
+    EPC_MODE_EXACT_SUMS = 1 << 14
 };
 int epc_set_mode(epc_context* ctx, int mode_bits);
+/* ADMM stop/rho decisions since the context was created: out2[0] taken on
+ * certified enclosures of the reference's sequential sums, out2[1] on the
+ * exact sequential sums (undecidable enclosure, or EPC_MODE_EXACT_SUMS). */
+int epc_decision_stats(epc_context* ctx, long long* out2);
 /* Phase cycle totals of the b-step kernel since timing was enabled (lane 0
  * clock64 deltas): model, fval sums, factor, solves, QP rest, KKT, step
  * sums, line search, clamp+store, column fetch. */
@@ -435,6 +444,15 @@ int epc_slab_zdiff(epc_context* ctx, const epc_grid* full, int k0, int mk, const
                    const double* halo, double* sums2);
 /* x *= factor (the u rescale after a rho change, admm.cpp:546-552). */
 int epc_slab_scale(epc_context* ctx, long long n, double* x, double factor);
+/* The reference's five sequential dual-update sums (sum (b-z)^2, (zo-z)^2,
+ * b^2, z^2, u^2 in index order, admm.cpp:461-469, grid.cpp:60-64) over n
+ * faces, continuing the chains in io5[5] (host, in/out). The slab loop calls
+ * it rank after rank when a certified decision is undecidable. */
+int epc_slab_seq_sums(epc_context* ctx, long long n, const double* b_new, const double* z_new,
+                      const double* z_old, const double* u_new, double* io5);
+/* max |D1 b| over the slab (admm_solve's feasibility check, admm.cpp:501-502). */
+int epc_slab_d1_norm_inf(epc_context* ctx, const epc_grid* full, int k0, int mk, const double* b,
+                         double* out);
 
 /* ---- GN-PCG in k-slabs (GN row) -------------------------------
  * Vectors are *extended*: the owned layers [k0, k0 + mk) plus one halo layer

@@ -17,6 +17,7 @@ EPC_ERR_UNSUPPORTED = 5
 EPC_MEM_HOST = 0
 EPC_MEM_DEVICE = 1
 
+STOP_CONVERGED, STOP_MAX_ITERATIONS, STOP_LINE_SEARCH_FAILURE, STOP_ERROR = 0, 1, 2, 3
 STOP_NAMES = {0: "converged", 1: "max_iterations", 2: "line_search_failure", 3: "error"}
 RHO_FIXED, RHO_ADAPTIVE, RHO_ADAPTIVE_BOUNDED = 0, 1, 2
 PRECOND_NONE, PRECOND_JACOBI, PRECOND_BLOCK_JACOBI, PRECOND_SGS = 0, 1, 2, 3

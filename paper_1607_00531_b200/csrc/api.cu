@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "admm_decide.h"
 
 namespace {
 
@@ -103,7 +104,7 @@ enum Slot {
     S_ML0, S_ML1, S_MLI, S_MLD, S_MLB, S_MLO, S_MLIP, S_MLIM, S_MLFIP, S_MLFIM,
     S_F32_IP, S_F32_IM, S_F32_B0, S_F32_B1, S_F32_Z0, S_F32_Z1, S_F32_U0, S_F32_U1, S_F32_T0,
     S_F32_T1, S_F32_MATS, S_F32_Q, S_F32_S, S_F32_COL, S_F32_SCAL, S_F32_PART,
-    S_CTIME,
+    S_CTIME, S_SEQ,
     S_COUNT
 };
 
@@ -142,6 +143,11 @@ void* pinned(epc_context* ctx, size_t bytes) {
 void h2d(epc_context* ctx, void* dst, const void* src, size_t bytes) {
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
 }
+void* pinned_aux(epc_context* ctx) {
+    if (!ctx->pinned_aux) CK(cudaMallocHost(&ctx->pinned_aux, 4096));
+    return ctx->pinned_aux;
+}
+
 void d2h(epc_context* ctx, void* dst, const void* src, size_t bytes) {
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
 }
@@ -572,6 +578,30 @@ double rho_schedule(int schedule, double rho, double rho_min, double pr, double 
     return next;
 }
 
+// rho_schedule's arithmetic (admm.cpp:478-486) for an already-taken decision
+// (move: +1 primal > mu dual, -1 dual > mu primal, 0 neither)
+double rho_apply(int schedule, double rho, double rho_min, int move, double ti, double td) {
+    if (schedule == EPC_RHO_FIXED) return rho;
+    double next = rho;
+    if (move > 0) next = rho * ti;
+    else if (move < 0) next = rho / td;
+    if (schedule == EPC_RHO_ADAPTIVE_BOUNDED) next = std::max(next, rho_min);
+    return next;
+}
+
+// The reference's five sequential sums (admm_decide.h fallback), read back.
+void seq_sums(epc_context* ctx, const double* b, const double* z, const double* zo,
+              const double* u, long long n, double out[5]) {
+    double* io = slot_t<double>(ctx, S_SEQ, 8);
+    CK(cudaMemsetAsync(io, 0, 5 * sizeof(double), ctx->stream));
+    run_seq_sums(ctx, b, z, zo, u, n, io);
+    check_launch();
+    double* h = static_cast<double*>(pinned_aux(ctx));
+    d2h(ctx, h, io, 5 * sizeof(double));
+    sync(ctx);
+    for (int i = 0; i < 5; ++i) out[i] = h[i];
+}
+
 // ---------------------------------------------------------------------------
 // ADMM solve over npairs pairs sharing a grid (admm.cpp:488-560)
 // ---------------------------------------------------------------------------
@@ -717,11 +747,36 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
                 row.rho = rho[q];
                 row.kkt_violation = cd[0];
                 row.b_update_s = bms * 1e-3;
-                // dual_update_and_residuals (admm.cpp:470-474)
-                row.primal_res = std::sqrt(du[0]);
-                row.dual_res = rho[q] * V * std::sqrt(du[1]);
-                row.eps_pri = sqrt_n * cfg->eps_abs + cfg->eps_rel * std::max(std::sqrt(du[2]), std::sqrt(du[3]));
-                row.eps_dual = sqrt_n * cfg->eps_abs + cfg->eps_rel * rho[q] * V * std::sqrt(du[4]);
+                // dual_update_and_residuals (admm.cpp:470-474) on the tree sums
+                const epc_decide::Res tr = epc_decide::residuals(du, rho[q], V, sqrt_n,
+                                                                 cfg->eps_abs, cfg->eps_rel);
+                row.primal_res = tr.pr;
+                row.dual_res = tr.du;
+                row.eps_pri = tr.eps_pri;
+                row.eps_dual = tr.eps_dual;
+                // stop test and rho schedule (admm.cpp:542-548): certified against the
+                // reference's sequential sums, else decided on those sums (admm_decide.h)
+                const bool adaptive = cfg->schedule != EPC_RHO_FIXED;
+                epc_decide::Decision dec{false, false, 0};
+                if (!(ctx->mode & EPC_MODE_EXACT_SUMS))
+                    dec = epc_decide::certified(du, g.nface, rho[q], V, sqrt_n, cfg->eps_abs,
+                                                cfg->eps_rel, cfg->mu, adaptive);
+                if (dec.decided) {
+                    ctx->dec_certified++;
+                } else {
+                    double seq[5];
+                    const size_t o = (size_t)q * g.nface;
+                    seq_sums(ctx, B[1] + o, Z[1] + o, Z[0] + o, U[1] + o, g.nface, seq);
+                    const epc_decide::Res ex = epc_decide::residuals(seq, rho[q], V, sqrt_n,
+                                                                     cfg->eps_abs, cfg->eps_rel);
+                    row.primal_res = ex.pr;  // now bitwise the reference's row values
+                    row.dual_res = ex.du;
+                    row.eps_pri = ex.eps_pri;
+                    row.eps_dual = ex.eps_dual;
+                    dec = epc_decide::exact(seq, rho[q], V, sqrt_n, cfg->eps_abs, cfg->eps_rel,
+                                            cfg->mu, adaptive);
+                    ctx->dec_exact++;
+                }
                 // augmented_lagrangian (admm.cpp:267-299)
                 const double fval = 0.5 * V * cd[1] + 0.5 * p->alpha * V * cd[2];
                 double gs = zd[0];
@@ -731,14 +786,14 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
                 row.wall_s = wall;
                 if (status[q].nrows < max_rows) rows[(size_t)q * max_rows + status[q].nrows] = row;
                 status[q].nrows++;
-                if (row.primal_res <= row.eps_pri && row.dual_res <= row.eps_dual) {
+                if (dec.converged) {
                     status[q].stop = EPC_STOP_CONVERGED;
                     active[q] = 0;
                     --n_active;
                     continue;
                 }
-                const double next = rho_schedule(cfg->schedule, rho[q], cfg->rho_min, row.primal_res,
-                                                 row.dual_res, cfg->tau_incr, cfg->tau_decr, cfg->mu);
+                const double next = rho_apply(cfg->schedule, rho[q], cfg->rho_min, dec.rho_move,
+                                              cfg->tau_incr, cfg->tau_decr);
                 if (next != rho[q]) {
                     fac[q] = rho[q] / next;
                     rho[q] = next;
@@ -921,6 +976,7 @@ void epc_context_destroy(epc_context* ctx) {
     for (auto& b : ctx->bufs)
         if (b.ptr) cudaFree(b.ptr);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->pinned_aux) cudaFreeHost(ctx->pinned_aux);
     for (auto& pe : ctx->prof_pending) {
         cudaEventDestroy(pe.start);
         cudaEventDestroy(pe.stop);
@@ -999,6 +1055,13 @@ void epc_profile_reset(epc_context* ctx) {
 }
 
 long epc_launch_count(const epc_context* ctx) { return ctx->launches; }
+
+int epc_decision_stats(epc_context* ctx, long long* out2) {
+    if (!ctx || !out2) return EPC_ERR_INVALID_ARGUMENT;
+    out2[0] = ctx->dec_certified;
+    out2[1] = ctx->dec_exact;
+    return EPC_OK;
+}
 void epc_reset_launch_count(epc_context* ctx) { ctx->launches = 0; }
 
 int epc_admm_solve(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,

@@ -77,3 +77,82 @@ __global__ void __launch_bounds__(256) k_dual_standalone(const double* b, const 
         __syncthreads();
     }
 }
+
+// The reference's five sequential sums of the dual update, in index order
+// (admm.cpp:461-469 and norm2 = sqrt(dot), grid.cpp:60-64): io[0..4] +=
+// sum (b-z)^2, sum (zo-z)^2, sum b^2, sum z^2, sum u^2 over i = 0..n-1, each
+// a one-thread chain (io carries a start value, so a chain can continue
+// across slabs in rank order). The fallback of the certified decisions
+// (admm_decide.h): warps 1.. form the terms of the next chunk in shared
+// memory (the same rounded products the reference adds) while thread 0 adds
+// the current chunk. One CTA of SEQ_THREADS threads.
+constexpr int SEQ_CHUNK = 1024;
+__global__ void __launch_bounds__(SEQ_THREADS) k_seq_sums(const double* b, const double* z,
+                                                          const double* zo, const double* u,
+                                                          long long n, double* io) {
+    extern __shared__ double seq_sh[];  // [2][5][SEQ_CHUNK]
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+    if (threadIdx.x == 0) {
+        s0 = io[0];
+        s1 = io[1];
+        s2 = io[2];
+        s3 = io[3];
+        s4 = io[4];
+    }
+    const long long nchunk = (n + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    auto fill = [&](long long c, double* buf) {
+        const long long base = c * SEQ_CHUNK;
+        for (int t = threadIdx.x - 32; t < SEQ_CHUNK; t += blockDim.x - 32) {
+            const long long i = base + t;
+            if (i >= n) break;
+            const double bi = b[i], zi = z[i];
+            const double diff = bi - zi;
+            const double dz = zo[i] - zi;
+            const double ui = u[i];
+            buf[t] = diff * diff;
+            buf[SEQ_CHUNK + t] = dz * dz;
+            buf[2 * SEQ_CHUNK + t] = bi * bi;
+            buf[3 * SEQ_CHUNK + t] = zi * zi;
+            buf[4 * SEQ_CHUNK + t] = ui * ui;
+        }
+    };
+    if (threadIdx.x >= 32 && nchunk > 0) fill(0, seq_sh);
+    __syncthreads();
+    for (long long c = 0; c < nchunk; ++c) {
+        double* cur = seq_sh + (c & 1) * 5 * SEQ_CHUNK;
+        double* nxt = seq_sh + ((c + 1) & 1) * 5 * SEQ_CHUNK;
+        if (threadIdx.x >= 32) {
+            if (c + 1 < nchunk) fill(c + 1, nxt);
+        } else if (threadIdx.x == 0) {
+            const long long cnt = min((long long)SEQ_CHUNK, n - c * SEQ_CHUNK);
+#pragma unroll 4
+            for (int t = 0; t < (int)cnt; ++t) {
+                s0 += cur[t];
+                s1 += cur[SEQ_CHUNK + t];
+                s2 += cur[2 * SEQ_CHUNK + t];
+                s3 += cur[3 * SEQ_CHUNK + t];
+                s4 += cur[4 * SEQ_CHUNK + t];
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        io[0] = s0;
+        io[1] = s1;
+        io[2] = s2;
+        io[3] = s3;
+        io[4] = s4;
+    }
+}
+size_t seq_sums_smem() { return 2 * 5 * SEQ_CHUNK * sizeof(double); }
+
+void run_seq_sums(epc_context* ctx, const double* b, const double* z, const double* zo,
+                  const double* u, long long n, double* io_dev) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_seq_sums, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)seq_sums_smem());
+        attr = true;
+    }
+    EPC_LAUNCH(ctx, "seq_sums", k_seq_sums, 1, SEQ_THREADS, seq_sums_smem(), b, z, zo, u, n, io_dev);
+}

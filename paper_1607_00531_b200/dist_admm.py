@@ -32,7 +32,7 @@ import math
 import time
 from dataclasses import dataclass
 
-from . import abi, shard
+from . import abi, decide, shard
 
 STOP_CONVERGED, STOP_MAX_ITER, STOP_ERROR = 0, 1, 3  # EPC_STOP_* (include/epicorr_b200.h)
 QP_WHAT = {1: "column factor: nonpositive pivot",
@@ -89,10 +89,13 @@ def rho_schedule(schedule, rho, rho_min, pr, du, ti, td, mu):
 
 
 def admm_rank(backend, grid, slabs, rank, ip, im, cfg=None, params=None, rho0=None, level_tag=0,
-              state=None):
+              state=None, exact_sums=False):
     """One rank of the distributed admm_solve (a generator; see module doc).
     ip / im: this rank's cell slab; state: optional (b, z, u) face slabs.
-    Returns dict(b, z, u, rho, rows, stop, message) for the rank's slab."""
+    exact_sums: take every stop / rho decision on the reference's sequential
+    sums (EPC_MODE_EXACT_SUMS), not only the undecidable ones.
+    Returns dict(b, z, u, rho, rows, stop, message, decisions) for the rank's
+    slab; decisions = [certified, exact]."""
     cfg = cfg or abi.AdmmConfig()
     params = params or abi.ObjectiveParams()
     world = slabs.world
@@ -115,8 +118,16 @@ def admm_rank(backend, grid, slabs, rank, ip, im, cfg=None, params=None, rho0=No
     recv_b = backend.zeros(nf)                      # rank blocks (return)
     fwd_send = [slabs.block(rank, s) for s in range(world)]
     fwd_recv = [slabs.block(s, rank) for s in range(world)]
+    if state is not None and state[0] is not None:
+        # admm.cpp:501-502: norm_inf(diff_x1(b)) > 1 throws before iteration 1
+        allm = yield ("gather", [backend.d1_norm_inf(grid, k0, mk, B[0])])
+        if max(v[0] for v in allm) > 1.0:
+            raise ValueError("admm_solve: infeasible starting field")
     rho = rho0 if (rho0 is not None and rho0 > 0.0) else cfg.rho0
     rows, stop, message = [], STOP_MAX_ITER, ""
+    ndec = [0, 0]
+    adaptive = cfg.schedule != abi.RHO_FIXED
+    nface_total = slabs.n1 * slabs.m2 * slabs.m3
     t0 = time.perf_counter()
     for it in range(1, cfg.max_iter + 1):
         tb = time.perf_counter()
@@ -156,11 +167,25 @@ def admm_rank(backend, grid, slabs, rank, ip, im, cfg=None, params=None, rho0=No
         row = abi.AdmmRow()
         row.level, row.iter, row.rho, row.kkt_violation = level_tag, it, rho, kkt
         row.b_update_s = bsec
-        row.primal_res = math.sqrt(du[0])
-        row.dual_res = rho * V * math.sqrt(du[1])
-        a2, a3 = math.sqrt(du[2]), math.sqrt(du[3])
-        row.eps_pri = sqrt_n * cfg.eps_abs + cfg.eps_rel * (a3 if a2 < a3 else a2)
-        row.eps_dual = sqrt_n * cfg.eps_abs + cfg.eps_rel * rho * V * math.sqrt(du[4])
+        row.primal_res, row.dual_res, row.eps_pri, row.eps_dual = decide.residuals(
+            du, rho, V, sqrt_n, cfg.eps_abs, cfg.eps_rel)
+        # stop test and rho schedule (admm.cpp:542-548), certified against the
+        # reference's sequential sums (decide.py); undecidable -> the exact
+        # chains, continued rank after rank in index order
+        dec = None if exact_sums else decide.certified(du, nface_total, rho, V, sqrt_n, cfg.eps_abs,
+                                                       cfg.eps_rel, cfg.mu, adaptive)
+        if dec is not None:
+            ndec[0] += 1
+        else:
+            seq = [0.0] * 5
+            for r in range(world):
+                if r == rank:
+                    seq = backend.seq_sums(B[1], Z[1], Z[0], U[1], seq)
+                seq = yield ("bcast", list(seq), r)
+            row.primal_res, row.dual_res, row.eps_pri, row.eps_dual = decide.residuals(
+                seq, rho, V, sqrt_n, cfg.eps_abs, cfg.eps_rel)
+            dec = decide.exact(seq, rho, V, sqrt_n, cfg.eps_abs, cfg.eps_rel, cfg.mu, adaptive)
+            ndec[1] += 1
         fval = 0.5 * V * fr + 0.5 * params.alpha * V * fd
         gs = zd[0] + (zd[1] if grid.dim == 3 else 0.0)
         gval = 0.5 * params.alpha * V * gs
@@ -170,15 +195,16 @@ def admm_rank(backend, grid, slabs, rank, ip, im, cfg=None, params=None, rho0=No
         B.reverse()
         Z.reverse()
         U.reverse()
-        if row.primal_res <= row.eps_pri and row.dual_res <= row.eps_dual:
+        if dec[0]:
             stop = STOP_CONVERGED
             break
-        nxt = rho_schedule(cfg.schedule, rho, cfg.rho_min, row.primal_res, row.dual_res,
-                           cfg.tau_incr, cfg.tau_decr, cfg.mu)
+        nxt = decide.rho_apply(cfg.schedule, rho, cfg.rho_min, dec[1], cfg.tau_incr, cfg.tau_decr,
+                               abi.RHO_FIXED, abi.RHO_ADAPTIVE_BOUNDED)
         if nxt != rho:
             backend.scale(U[0], rho / nxt)
             rho = nxt
-    return dict(b=B[0], z=Z[0], u=U[0], rho=rho, rows=rows, stop=stop, message=message)
+    return dict(b=B[0], z=Z[0], u=U[0], rho=rho, rows=rows, stop=stop, message=message,
+                decisions=ndec)
 
 
 # ---------------------------------------------------------------------------
@@ -218,6 +244,9 @@ def run_lockstep(gens, cat, split):
         elif kind == "gather":
             vals = [list(r[1]) for r in reqs]
             answers = [vals] * world
+        elif kind == "bcast":
+            root = reqs[0][2]
+            answers = [list(reqs[root][1])] * world
         else:
             raise RuntimeError(kind)
         nxt = []
@@ -288,6 +317,10 @@ def run_torch(gen, dist, device):
                 outs = [torch.empty_like(t) for _ in range(world)]
                 dist.all_gather(outs, t)
                 ans = [o.cpu().tolist() for o in outs]
+            elif kind == "bcast":
+                t = torch.tensor(req[1], dtype=torch.float64, device=device)
+                dist.broadcast(t, src=req[2])
+                ans = t.cpu().tolist()
             else:
                 raise RuntimeError(kind)
             req = gen.send(ans)
@@ -378,6 +411,21 @@ class DeviceBackend:
         self.ctx._check(self.lib.epc_slab_zdiff(self.ctx.h, C.byref(g), k0, mk, self._p(z),
                                                 self._p(halo), s2))
         return list(s2)
+
+    def seq_sums(self, b_new, z_new, z_old, u_new, start):
+        self._sync_torch()
+        io = (C.c_double * 5)(*start)
+        self.ctx._check(self.lib.epc_slab_seq_sums(self.ctx.h, b_new.numel(), self._p(b_new),
+                                                   self._p(z_new), self._p(z_old), self._p(u_new),
+                                                   io))
+        return list(io)
+
+    def d1_norm_inf(self, g, k0, mk, b):
+        self._sync_torch()
+        out = C.c_double(0.0)
+        self.ctx._check(self.lib.epc_slab_d1_norm_inf(self.ctx.h, C.byref(g), k0, mk, self._p(b),
+                                                      C.byref(out)))
+        return out.value
 
     def scale(self, x, factor):
         self.ctx._check(self.lib.epc_slab_scale(self.ctx.h, x.numel(), self._p(x), factor))

@@ -134,6 +134,14 @@ class Context:
                       "acc32_39", "fail", "schur_n", "schur_na", "schur_na2", "schur_na3"]
     MODE_BSTEP_TIMING = 1
     MODE_BSTEP_CHAINED = 1 << 13
+    MODE_EXACT_SUMS = 1 << 14
+
+    def decision_stats(self):
+        """ADMM stop/rho decisions so far: (certified from the tree sums,
+        taken on the reference's exact sequential sums)."""
+        out = (C.c_longlong * 2)()
+        self._check(self.lib.epc_decision_stats(self.h, out))
+        return int(out[0]), int(out[1])
 
     def bstep_counters(self):
         out = (C.c_longlong * 18)()
@@ -207,17 +215,21 @@ class Context:
                     rows=abi.rows_to_dicts(rows, min(st.nrows, cfg.max_iter)))
 
     def admm_solve_batch(self, g: Grid, npairs, ip, im, rho=None, params=None, cfg=None,
-                         level_tag=0):
+                         level_tag=0, b=None, z=None, u=None):
+        """npairs independent admm_solve calls on one grid in the same kernels
+        (pair-major arrays; b/z/u: optional warm starts for every pair, rho:
+        per-pair start values, <= 0 selects rho0). Returns dict(b, z, u, pairs)."""
         params = params or ObjectiveParams()
         cfg = cfg or AdmmConfig()
-        mem = self._mem(ip, im)
+        mem = self._mem(ip, im, b, z, u)
         nf = g.faces * npairs
         bo, zo, uo = self._like(ip, nf), self._like(ip, nf), self._like(ip, nf)
         rows = (AdmmRow * (max(cfg.max_iter, 1) * npairs))()
         st = (SolveStatus * npairs)()
         rh = (C.c_double * npairs)(*([0.0] * npairs if rho is None else rho))
         rc = self.lib.epc_admm_solve_batch(self.h, C.byref(g), npairs, mem, self._ptr(ip),
-                                           self._ptr(im), None, None, None, self._ptr(bo),
+                                           self._ptr(im), self._ptr(b), self._ptr(z), self._ptr(u),
+                                           self._ptr(bo),
                                            self._ptr(zo), self._ptr(uo), rh, C.byref(params),
                                            C.byref(cfg), level_tag, rows, cfg.max_iter, st)
         if rc != 0:

@@ -22,7 +22,11 @@
 // symbols renamed by -D at compile time).
 //
 // Device: EPICORR_B200_DEVICE (default 0); one context per process, created
-// on first use, owning its stream.
+// on first use, owning its stream. Threading: the reference's free functions
+// may be called from several host threads at once; every entry point here
+// holds one process-wide lock for its whole call (the context's scratch
+// slots, pinned staging and stream are shared), so concurrent callers are
+// serialised on the one device instead of corrupting each other.
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -36,6 +40,12 @@
 #include "epicorr_b200.h"
 
 namespace {
+
+std::recursive_mutex& shim_mutex() {
+    static std::recursive_mutex m;
+    return m;
+}
+#define SHIM_LOCK std::lock_guard<std::recursive_mutex> shim_lock_(shim_mutex())
 
 epc_context* ctx() {
     static std::once_flag once;
@@ -118,10 +128,18 @@ namespace epicorr {
 
 AdmmSolveResult admm_solve(const VolumePair& pair, ADMMState init, const ObjectiveParams& params,
                            const ADMMConfig& config, int level_tag) {
+    SHIM_LOCK;
     const GridSpec& g = pair.grid();
     const epc_grid cg = to_c(g);
     const epc_objective_params cp = to_c(params);
     const epc_admm_config cc = to_c(config);
+    // admm.cpp:490-498, in the reference's order (a field on another grid
+    // would otherwise be over-read by the ABI)
+    params.validate();
+    config.validate();
+    if ((!init.b.v.empty() && !(init.b.grid == g)) || (!init.z.v.empty() && !(init.z.grid == g)) ||
+        (!init.u.v.empty() && !(init.u.grid == g)))
+        throw std::invalid_argument("admm_solve: state grids do not match the pair");
     AdmmSolveResult out;
     out.state.b = StaggeredField(g);
     out.state.z = StaggeredField(g);
@@ -161,6 +179,7 @@ AdmmSolveResult admm_solve(const VolumePair& pair, ADMMState init, const Objecti
 
 StaggeredField b_update(const VolumePair& pair, const ADMMState& state, const ObjectiveParams& params,
                         const ADMMConfig& config, BUpdateStats* stats) {
+    SHIM_LOCK;
     const GridSpec& g = pair.grid();
     if (!(state.b.grid == g) || !(state.z.grid == g) || !(state.u.grid == g))
         throw std::invalid_argument("b_update: state grids do not match the pair");
@@ -181,6 +200,7 @@ StaggeredField b_update(const VolumePair& pair, const ADMMState& state, const Ob
 }
 
 StaggeredField z_update(const ADMMState& state, double alpha, const DctCoupledSolver&) {
+    SHIM_LOCK;
     const GridSpec& g = state.b.grid;
     const epc_grid cg = to_c(g);
     StaggeredField out(g);
@@ -192,6 +212,7 @@ StaggeredField z_update(const ADMMState& state, double alpha, const DctCoupledSo
 DualUpdate dual_update_and_residuals(const StaggeredField& b_new, const StaggeredField& z_new,
                                      const StaggeredField& z_old, const StaggeredField& u_old,
                                      double rho, double eps_abs, double eps_rel) {
+    SHIM_LOCK;
     const GridSpec& g = b_new.grid;
     if (!(z_new.grid == g) || !(z_old.grid == g) || !(u_old.grid == g))
         throw std::invalid_argument("dual_update_and_residuals: grid mismatch");
@@ -210,6 +231,7 @@ DualUpdate dual_update_and_residuals(const StaggeredField& b_new, const Staggere
 
 double augmented_lagrangian(const VolumePair& pair, const StaggeredField& b, const StaggeredField& z,
                             const StaggeredField& u, double rho, double alpha, int) {
+    SHIM_LOCK;
     const epc_grid cg = to_c(pair.grid());
     double v = 0.0;
     check(epc_augmented_lagrangian(ctx(), &cg, EPC_MEM_HOST, pair.plus.v.data(),
@@ -220,6 +242,7 @@ double augmented_lagrangian(const VolumePair& pair, const StaggeredField& b, con
 
 QpResult qp_active_set(int n, double h, std::span<const double> gdiag, std::span<const double> goff,
                        std::span<const double> c, std::span<const double> x0, int max_iter) {
+    SHIM_LOCK;
     QpResult r;
     r.x.assign(n, 0.0);
     r.lambda.assign(n - 1, 0.0);
@@ -237,6 +260,7 @@ QpResult qp_active_set(int n, double h, std::span<const double> gdiag, std::span
 GnSolveResult gauss_newton_solve(const VolumePair& pair, const StaggeredField& b0,
                                  const ObjectiveParams& params, const GNConfig& config,
                                  int level_tag) {
+    SHIM_LOCK;
     const GridSpec& g = pair.grid();
     if (!(b0.grid == g)) throw std::invalid_argument("gauss_newton_solve: grid mismatch");
     const epc_grid cg = to_c(g);
@@ -264,6 +288,7 @@ GnSolveResult gauss_newton_solve(const VolumePair& pair, const StaggeredField& b
 
 // ---- multilevel (multilevel.hpp:37-63) on the device --------------------------
 ImageVolume restrict_image(const ImageVolume& img, const GridSpec& coarse) {
+    SHIM_LOCK;
     const epc_grid cf = to_c(img.grid), cc = to_c(coarse);
     coarse.validate();
     ImageVolume out(coarse);
@@ -272,6 +297,7 @@ ImageVolume restrict_image(const ImageVolume& img, const GridSpec& coarse) {
 }
 
 StaggeredField prolong_field(const StaggeredField& b_coarse, const GridSpec& fine) {
+    SHIM_LOCK;
     const epc_grid cc = to_c(b_coarse.grid), cf = to_c(fine);
     fine.validate();
     StaggeredField out(fine);
@@ -283,6 +309,7 @@ MultilevelResult multilevel_solve(const VolumePair& pair, const LevelSchedule& s
                                   SolverKind solver, const ObjectiveParams& params,
                                   const GNConfig& gn_config, const ADMMConfig& admm_config,
                                   AdmmRestart restart) {
+    SHIM_LOCK;
     schedule.validate();
     const int nlev = schedule.levels();
     std::vector<epc_grid> lv;

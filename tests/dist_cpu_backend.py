@@ -61,6 +61,17 @@ class OracleBackend:
     def view(self, x, first, n):
         return x[first:first + n]
 
+    def seq_sums(self, b_new, z_new, z_old, u_new, start):
+        """The reference's sequential chains (np.add.accumulate adds in index
+        order, one rounding per element), continued from start."""
+        terms = [(b_new - z_new) ** 2, (z_old - z_new) ** 2, b_new * b_new, z_new * z_new,
+                 u_new * u_new]
+        return [float(np.add.accumulate(np.concatenate(([s0], t)))[-1]) for s0, t in zip(start, terms)]
+
+    def d1_norm_inf(self, g, k0, mk, b):
+        bb = b.reshape(-1, g.m[0] + 1)
+        return float(np.abs((bb[:, 1:] - bb[:, :-1]) * (1.0 / g.h[0])).max())  # diff_x1, operators.cpp:45-49
+
     def bstep(self, g, k0, mk, ip, im, b, z, u, rho, params, cfg, b_out):
         sg = self._slab_grid(mk)
         r = self.orc.b_update(sg, ip, im, b, z, u, rho, params=params, cfg=cfg)

@@ -80,7 +80,60 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_lockstep_exact_sums_rows_bitwise(oracle, world):
+    """Every decision on the reference's sequential sums, chained rank after
+    rank in index order (decide.py fallback): the rows' residuals are then
+    bitwise the reference's, and b, z, u still are."""
+    from dist_cpu_backend import OracleBackend, np_cat, np_split
+    g, ip, im = _pair()
+    cfg = abi.AdmmConfig(max_iter=ITERS, **EXACT)
+    slabs = dist_admm.Slabs(*M, world)
+    gens = []
+    for r in range(world):
+        sip, sim = _slab_inputs(g, ip, im, slabs, r)
+        gens.append(dist_admm.admm_rank(OracleBackend(oracle, g), g, slabs, r, sip, sim, cfg=cfg,
+                                        exact_sums=True))
+    res = dist_admm.run_lockstep(gens, np_cat, np_split)
+    _check_against_oracle(oracle, g, ip, im, res, slabs, cfg)
+    ref = oracle.admm_solve(g, ip, im, cfg=cfg)
+    for r in res:
+        assert r["decisions"] == [0, ITERS]
+        for a, b in zip(r["rows"], ref["rows"]):
+            for f in ("primal_res", "dual_res", "eps_pri", "eps_dual"):
+                assert getattr(a, f) == b[f], f
+
+
+def test_lockstep_default_tolerances_and_infeasible_start(oracle):
+    """Default eps (the stop test fires at iteration 1) through
+    the certified decisions; an infeasible starting field raises the
+    reference's invalid_argument before iteration 1 (admm.cpp:501-502)."""
+    from dist_cpu_backend import OracleBackend, np_cat, np_split
+    g, ip, im = _pair()
+    world = 2
+    slabs = dist_admm.Slabs(*M, world)
+    cfg = abi.AdmmConfig(max_iter=ITERS)
+    gens = []
+    for r in range(world):
+        sip, sim = _slab_inputs(g, ip, im, slabs, r)
+        gens.append(dist_admm.admm_rank(OracleBackend(oracle, g), g, slabs, r, sip, sim, cfg=cfg))
+    res = dist_admm.run_lockstep(gens, np_cat, np_split)
+    _check_against_oracle(oracle, g, ip, im, res, slabs, cfg)
+    bad = np.zeros(g.faces)
+    bad.reshape(-1, g.m[0] + 1)[3, 5] = 1.5  # |D1 b| = 1.5 > 1
+    gens = []
+    for r in range(world):
+        sip, sim = _slab_inputs(g, ip, im, slabs, r)
+        k0, mk = slabs.k_range(r)
+        lay = (g.m[0] + 1) * g.m[1]
+        st = (np.ascontiguousarray(bad[k0 * lay:(k0 + mk) * lay]), None, None)
+        gens.append(dist_admm.admm_rank(OracleBackend(oracle, g), g, slabs, r, sip, sim, cfg=cfg,
+                                        state=st))
+    with pytest.raises(ValueError, match="infeasible starting field"):
+        dist_admm.run_lockstep(gens, np_cat, np_split)
+
+
+def _worker(rank, world, port, q, exact_sums=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -94,7 +147,7 @@ def _worker(rank, world, port, q):
         slabs = dist_admm.Slabs(*M, world)
         sip, sim = _slab_inputs(g, ip, im, slabs, rank)
         gen = dist_admm.admm_rank(OracleBackend(ffi.load("oracle"), g), g, slabs, rank, sip, sim,
-                                  cfg=cfg)
+                                  cfg=cfg, exact_sums=exact_sums)
         out = dist_admm.run_torch(gen, dist, torch.device("cpu"))
         rows = [(x.iter, x.rho, x.kkt_violation, x.primal_res, x.dual_res, x.lagrangian)
                 for x in out["rows"]]
@@ -103,12 +156,13 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_gloo_two_ranks_match_reference(oracle):
+@pytest.mark.parametrize("exact_sums", [False, True])
+def test_gloo_two_ranks_match_reference(oracle, exact_sums):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, exact_sums)) for r in range(world)]
     for p in procs:
         p.start()
     got = sorted([q.get(timeout=240) for _ in range(world)], key=lambda t: t[0])
