@@ -58,17 +58,19 @@ def parse():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--iters", type=int, default=None, help="ADMM iterations per solve")
     ap.add_argument("--scale", type=float, default=1.0, help="intensity scale (x400 variant)")
-    ap.add_argument("--ref-iters", type=int, default=2, help="ADMM iterations per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gn", action="store_true", help="skip the GN-PCG leg (configs[1])")
     ap.add_argument("--gn-config", default="C2")
     ap.add_argument("--no-f32", action="store_true", help="skip the fp32-variant leg")
+    ap.add_argument("--no-gn-c3", action="store_true", help="skip the GN-PCG C3 leg")
+    ap.add_argument("--no-x400", action="store_true", help="skip the amplitude-x400 C3 leg")
     return ap.parse_args()
 
 
 # fp64 DADD/DMUL issue rate measured on this pool (profiles/r01_ubench_fp64_tput.log)
 FP64_PEAK_TOPS = 18.3
 NCU_BSTEP_SUMMARY = "r01o_bstep_ncu.json"  # C3 b-step, one launch, ncu --set full
+NCU_PCG_SUMMARY = {"C2": "r02_pcg_c2_ncu.json", "C3": "r02_pcg_c3_ncu.json"}  # k_pcg_loop captures
 DEFAULT_ITERS = {"C1": 50, "C2": 50, "C3": 100, "C4": 50, "C5": 50}
 
 
@@ -141,19 +143,79 @@ def dist_setup(n):
     return rank, world, local, dist
 
 
-def cpu_reference(d, iters, threads):
-    """Reference CPU implementation (oracle/_ref) if built, else the C port."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def ref_checker(threads):
+    """The reference's CPU implementation: oracle/_ref (proj/src compiled
+    unmodified) when built, else the single-threaded C port (oracle/_build).
+    -> (checker, kind, cores)."""
     from oracle import ffi
     kind = "reference" if os.path.exists(ffi.PATHS["ref"]) else "port"
     chk = ffi.load("ref" if kind == "reference" else "oracle")
+    cores = threads if kind == "reference" else 1
     if kind == "reference":
-        chk.set_threads(threads)
-    cfg = abi.AdmmConfig(max_iter=iters, eps_abs=1e-300, eps_rel=1e-300,
-                         threads=threads if kind == "reference" else 1)
+        chk.set_threads(cores)
+    return chk, kind, cores
+
+
+def admm_cfg(iters, threads=1):
+    return abi.AdmmConfig(max_iter=iters, eps_abs=1e-300, eps_rel=1e-300, threads=threads)
+
+
+def ref_admm_window(chk, cores, d, state, n):
+    """n reference ADMM iterations warm-started from state (b, z, u, rho) via
+    ADMMState init (admm.hpp:127-129; the mechanism multilevel.cpp:252 uses),
+    which continues the trajectory exactly (eps = 1e-300: no stop test fires).
+    -> (seconds, b_update seconds, result)."""
+    kw = {} if state is None else dict(b=state["b"], z=state["z"], u=state["u"], rho=state["rho"])
     t = time.perf_counter()
-    chk.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
+    r = chk.admm_solve(d.grid, d.iplus, d.iminus, cfg=admm_cfg(n, cores), **kw)
     dt = time.perf_counter() - t
-    return kind, dt, (threads if kind == "reference" else 1)
+    return dt, sum(x["b_update_s"] for x in r["rows"]), r
+
+
+def window_sizes(total, k):
+    """k consecutive windows covering `total` iterations (cycled when k > total)."""
+    if k <= total:
+        return [(s * total) // k for s in range(k + 1)]
+    return None
+
+
+def ref_trajectory(chk, cores, d, iters, steps):
+    """The whole iters-long solve timed as `steps` consecutive windows, each
+    warm-started from the previous one's state: every timed step is a
+    bounded slice and together they are exactly one full solve (restarted
+    from b = 0 when steps > iters). -> (seconds, b_update seconds, faces x
+    iterations, per-window list, mid-trajectory state, its iteration)."""
+    bounds = window_sizes(iters, steps)
+    sizes = ([bounds[s + 1] - bounds[s] for s in range(steps)] if bounds is not None
+             else [1] * steps)
+    state, done = None, 0
+    tot = tb = 0.0
+    units = 0
+    wins = []
+    mid, mid_it = None, 0
+    for n in sizes:
+        if done >= iters:
+            state, done = None, 0
+        if mid is None and done >= iters // 2:
+            mid, mid_it = state, done
+        dt, bt, r = ref_admm_window(chk, cores, d, state, n)
+        state = r
+        done += n
+        tot += dt
+        tb += bt
+        units += d.grid.faces * n
+        wins.append({"first_iter": done - n + 1, "iters": n, "s": round(dt, 4)})
+    return tot, tb, units, wins, mid, mid_it
 
 
 def run_reference_arm(a, iters):
@@ -162,39 +224,60 @@ def run_reference_arm(a, iters):
         return 0
     d = synth.make_config(a.config, scale=a.scale)
     threads = os.cpu_count() or 1
-    times = []
-    kind = cores = None
-    for s in range(a.warmup + a.steps):
-        kind, dt, cores = cpu_reference(d, a.ref_iters, threads)
-        if s >= a.warmup:
-            times.append(dt)
-    t = float(np.mean(times))
-    value = d.grid.faces * a.ref_iters / t
+    chk, kind, cores = ref_checker(threads)
+    for _ in range(a.warmup):  # one iteration from b = 0 each (page-in, thread pools)
+        ref_admm_window(chk, cores, d, None, 1)
+    tot, tb, units, wins, mid, mid_it = ref_trajectory(chk, cores, d, iters, a.steps)
+    value = units / tot
+    # a 1-thread figure: the iteration after the mid-trajectory window boundary
+    one = None
+    if kind == "reference" and mid is not None:
+        try:
+            chk.set_threads(1)
+            dt1, _, _ = ref_admm_window(chk, 1, d, mid, 1)
+            one = {"value": d.grid.faces / dt1, "unit": UNIT, "cores": 1,
+                   "sample": f"ADMM iteration {mid_it + 1} of the {a.config} solve, 1 thread"}
+        except Exception as e:  # diagnostic only
+            one = {"value": None, "sample": str(e)[:120]}
+        finally:
+            chk.set_threads(cores)
     line = {"metric": metric_for(a.config), "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "warmup": a.warmup, "ms_per_step": tot / a.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"ADMM {a.config} {'x'.join(map(str, d.grid.dims()))}",
-                       "iterations_per_step": a.ref_iters, "full_solve_iterations": iters,
-                       "intensity_scale": a.scale},
+            "config": admm_config_dict(a, d.grid, iters),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": f"{a.ref_iters} ADMM iterations of the {a.config} solve per step"},
+                             "cpu_model": cpu_model(),
+                             "sample": (f"the whole {iters}-iteration {a.config} solve from b = 0, "
+                                        f"timed as {a.steps} consecutive warm-started windows "
+                                        f"(ADMMState init)"),
+                             "time_to_solution_s": tot * iters / max(1, sum(w["iters"] for w in wins)),
+                             "phase_split": {"b_update_s": tb, "z_dual_lagrangian_s": tot - tb,
+                                             "b_update_frac": tb / tot},
+                             "one_thread": one,
+                             "windows": wins},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     if not a.no_gn:
         dg = synth.make_config(a.gn_config)
-        vals = []
-        for s_ in range(a.warmup + a.steps):
-            kind, dt, cores, npcg = gn_reference_sample(dg, threads)
-            if s_ >= a.warmup:
-                vals.append(dg.grid.faces * npcg / dt)
-        v = float(np.mean(vals))
+        gt = gn_reference_trajectory(dg, threads, a.steps)
         line["gn"] = {"metric": f"voxel-iterations/s (GN-PCG, {'x'.join(map(str, dg.grid.dims()))}, fp64)",
-                      "value": v, "unit": GN_UNIT,
-                      "cpu_baseline": {"value": v, "unit": GN_UNIT, "cores": cores, "kind": kind,
-                                       "sample": f"1 GN step (<=50 PCG iterations) of the {a.gn_config} solve per step"},
-                      "e2e": {"value": v, "unit": GN_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                      "value": gt["value"], "unit": GN_UNIT,
+                      "cpu_baseline": gt,
+                      "e2e": {"value": gt["value"], "unit": GN_UNIT, "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def admm_config_dict(a, g, iters):
+    """The `config` object, identical in both arms (same workload)."""
+    return {"workload": f"ADMM {a.config} {'x'.join(map(str, g.dims()))}, {iters} iterations, "
+                        f"fp64, from b=0",
+            "faces": g.faces, "iterations": iters, "intensity_scale": a.scale,
+            "pairs": 64 if a.config == "C4" else 1,
+            "parallelism": ("pairs sharded over ranks" if a.config == "C4"
+                            else "one volume per GPU (replicas)"),
+            "l2": "working set > L2 (126 MB); the GPU arm also writes 256 MB before every timed step"}
 
 
 GN_UNIT = "face-PCG-iterations/s"
@@ -208,33 +291,50 @@ def gn_config():
                         eps_grad=1e-300, precond=abi.PRECOND_BLOCK_JACOBI)
 
 
-def gn_reference_sample(d, threads, outer=1):
+def gn_reference_sample(d, threads, outer=1, b0=None):
     """The reference's GN (oracle/_ref, else the C port) for `outer` GN steps
-    of the configs[1] solve -> (kind, seconds, cores, PCG iterations)."""
-    from oracle import ffi
-    kind = "reference" if os.path.exists(ffi.PATHS["ref"]) else "port"
-    chk = ffi.load("ref" if kind == "reference" else "oracle")
+    of the configs[1] solve from b0 -> (kind, seconds, cores, PCG iterations, b)."""
+    chk, kind, cores = ref_checker(threads)
     cfg = gn_config()
     cfg.max_outer = outer
-    if kind == "reference":
-        chk.set_threads(threads)
-        cfg.threads = threads
+    cfg.threads = cores
     t = time.perf_counter()
-    r = chk.gn_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
+    r = chk.gn_solve(d.grid, d.iplus, d.iminus, b0=b0, cfg=cfg)
     dt = time.perf_counter() - t
     npcg = sum(x["pcg_iters"] for x in r["rows"])
-    return kind, dt, (threads if kind == "reference" else 1), npcg
+    return kind, dt, cores, npcg, r["b"]
 
 
-def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
-    """GN-PCG on configs[1] (C2 128x128x64): device-resident time to solution
-    and face-PCG-iterations/s, e2e through the C ABI with host buffers, the
-    PCG kernels against the HBM roof, and the reference CPU sample beside it."""
+def gn_reference_trajectory(d, threads, steps, outer_total=10):
+    """The reference's whole 10-step GN solve, timed one GN step per window
+    (warm-started from the previous b; the stopping tests are off, so the
+    trajectory is the one-call solve's), cycled to fill `steps` windows."""
+    b, done, tot, npcg = None, 0, 0.0, 0
+    kind = cores = None
+    for _ in range(max(steps, 1)):
+        if done >= outer_total:
+            b, done = None, 0
+        kind, dt, cores, n, b = gn_reference_sample(d, threads, 1, b)
+        done += 1
+        tot += dt
+        npcg += n
+    return {"value": d.grid.faces * npcg / tot, "unit": GN_UNIT, "cores": cores, "kind": kind,
+            "sample": (f"the {outer_total}-step {'x'.join(map(str, d.grid.dims()))} GN solve, one "
+                       f"GN step per window, {max(steps, 1)} windows"),
+            "pcg_iterations": npcg, "seconds": tot}
+
+
+def run_gn_leg(a, ctx, dev, stream, flush, rank, dist, config_name, cpu_windows, min_solves=10):
+    """GN-PCG (configs[1] on C2 128x128x64, and the north-star target on C3
+    256x256x96): device-resident time to solution and face-PCG-iterations/s,
+    e2e through the C ABI with host buffers, the PCG kernels against the HBM
+    roof (with the ncu DRAM traffic when a capture summary is committed), and
+    the reference CPU sample beside it (cpu_windows GN steps of the solve)."""
     import ctypes as C
 
     import torch
     from dataclasses import replace
-    spec = synth.CONFIGS[a.gn_config]
+    spec = synth.CONFIGS[config_name]
     spec = replace(spec, seed=spec.seed + 1000 * rank)
     d = synth.make_pair(spec)
     g = d.grid
@@ -277,7 +377,7 @@ def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
 
     # a GN solve is ~25 ms with 10 host round trips: time at least 10 solves
     # so host scheduling jitter averages out
-    gk = max(a.steps, 10)
+    gk = max(a.steps, min_solves)
     for _ in range(max(a.warmup, 3)):
         solve_device()
     t_dev, launches, npcg = timed(solve_device, gk)
@@ -315,32 +415,143 @@ def run_gn_leg(a, ctx, dev, stream, flush, rank, dist):
         kernels.append(k)
     roof = None
     top = next((k for k in kernels if "achieved_gbs" in k), None)
+    fits_l2 = 15 * 8 * g.faces < 126e6
     if top is not None:
         try:
             peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
             src = "measured"
         except Exception:
             peak, src = 6650.0, "fallback"
+        traffic, tsrc = None, None
+        cap_name = NCU_PCG_SUMMARY.get(config_name)
+        try:  # DRAM bytes per PCG iteration of the loop kernel from the committed capture
+            cap = json.load(open(os.path.join(ROOT, "profiles", cap_name)))
+            traffic = float(cap["dram_bytes_per_pcg_iteration"])
+            tsrc = "profiles/" + cap_name
+        except Exception:
+            pass
         roof = {"bound": "hbm", "kernel": top["kernel"], "achieved": top["achieved_gbs"], "peak": peak,
-                "peak_source": src, "unit": "GB/s", "frac": top["achieved_gbs"] / peak, "traffic": None,
-                "note": "algorithmic bytes (120 B/face per PCG iteration) / CUDA-event time; "
-                        "C2 vectors are 8.5 MB, so launch ramp and grid barriers weigh"}
+                "peak_source": src, "unit": "GB/s", "frac": top["achieved_gbs"] / peak,
+                "traffic": traffic, "traffic_unit": "bytes per PCG iteration",
+                "alg_bytes_per_pcg_iteration": 120 * g.faces, "traffic_source": tsrc,
+                "note": ("algorithmic bytes (120 B/face per PCG iteration) / CUDA-event time; " +
+                         ("the PCG vectors fit in L2 at this size" if fits_l2 else
+                          "the PCG vectors (~15 face vectors) exceed L2: HBM-resident"))}
     out = {"metric": f"voxel-iterations/s (GN-PCG, {'x'.join(map(str, g.dims()))}, fp64)",
            "value": g.faces * npcg / t_dev * world, "unit": GN_UNIT,
            "steps": gk, "time_to_solution_s": t_dev / gk, "pcg_iterations_per_solve": npcg // gk,
-           "workload": f"GN-PCG {a.gn_config} block-Jacobi, 10 GN steps x <=50 PCG, eta 1e-2",
+           "workload": f"GN-PCG {config_name} block-Jacobi, 10 GN steps x <=50 PCG, eta 1e-2",
            "e2e": {"value": g.faces * npcg_h / t_e2e * world, "unit": GN_UNIT,
                    "h2d_bytes_per_step": (2 * g.cells + g.faces) * 8,
                    "d2h_bytes_per_step": g.faces * 8},
            "gpu_launches": launches, "roofline": roof, "kernels": kernels[:8],
-           "l2": "256 MB flush write before every timed step; the C2 PCG vectors (~85 MB) "
-                 "fit in L2 within a solve"}
+           "l2": "256 MB flush write before every timed step"}
     if rank == 0 and not a.no_cpu_baseline:
         try:
-            kind, dt, cores, np_ = gn_reference_sample(d, os.cpu_count() or 1)
-            out["cpu_baseline"] = {"value": g.faces * np_ / dt, "unit": GN_UNIT, "cores": cores,
-                                   "kind": kind, "sample": "1 GN step (<=50 PCG iterations) "
-                                                           f"of the {a.gn_config} solve"}
+            out["cpu_baseline"] = gn_reference_trajectory(d, os.cpu_count() or 1, cpu_windows)
+        except Exception as e:
+            out["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(e)[:120]}
+    return out
+
+
+def gpu_checkpoints(ctx, g, ip_d, im_d, starts, params=None):
+    """Host copies of the ADMM state at the given iteration counts, from the
+    device solve (b, z, u, rho are bitwise the reference's trajectory:
+    tests/test_gpu_fullsize.py), so CPU windows can start mid-trajectory."""
+    out, st, done = {}, None, 0
+    for s_ in sorted(set(starts)):
+        if s_ > done:
+            kw = {} if st is None else dict(b=st["b"], z=st["z"], u=st["u"], rho=st["rho"])
+            st = ctx.admm_solve(g, ip_d, im_d, cfg=admm_cfg(s_ - done), params=params, **kw)
+            done = s_
+        out[s_] = None if st is None else dict(
+            b=st["b"].double().cpu().numpy(), z=st["z"].double().cpu().numpy(),
+            u=st["u"].double().cpu().numpy(), rho=st["rho"])
+    return out
+
+
+def cpu_windows_baseline(ctx, d, ip_d, im_d, iters, config, starts, n):
+    """cpu_baseline: the reference (oracle/_ref, all host threads) timed on n
+    iterations starting at each of `starts` (states from gpu_checkpoints):
+    a bounded sample spread evenly over the whole trajectory."""
+    threads = os.cpu_count() or 1
+    chk, kind, cores = ref_checker(threads)
+    cps = gpu_checkpoints(ctx, d.grid, ip_d, im_d, starts)
+    tot, units = 0.0, 0
+    for s_ in starts:
+        dt, _, _ = ref_admm_window(chk, cores, d, cps[s_], n)
+        tot += dt
+        units += d.grid.faces * n
+    return {"value": units / tot, "unit": UNIT, "cores": cores, "kind": kind,
+            "cpu_model": cpu_model(),
+            "sample": (f"{n} ADMM iterations from each of iterations {[x + 1 for x in starts]} "
+                       f"of the {iters}-iteration {config} solve (warm-started through "
+                       f"ADMMState init), {units // d.grid.faces} iterations in all"),
+            "seconds": tot}
+
+
+def run_x400_leg(a, ctx, dev, stream, flush, iters, rank, dist):
+    """The amplitude-x400 variant of C3 (image.hpp:87-90: the
+    reference's phantoms use 400 so the distance term dominates alpha = 50):
+    time per solve, b-step ms per launch, and the SQP / QP / line-search
+    work counters, beside a reference CPU sample."""
+    import torch
+    from dataclasses import replace
+    spec = synth.CONFIGS[a.config]
+    spec = replace(spec, scale=400.0, seed=spec.seed + 1000 * rank)
+    d = synth.make_pair(spec)
+    g = d.grid
+    ip_d, im_d = torch.from_numpy(d.iplus).to(dev), torch.from_numpy(d.iminus).to(dev)
+    cfg = admm_cfg(iters)
+    ctx.admm_solve(g, ip_d, im_d, cfg=cfg)
+    k = max(1, min(a.steps, 5))
+    tot = 0.0
+    launches = 0
+    c0 = ctx.admm_counters()
+    for _ in range(k):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx.reset_launch_count()
+        e0.record(stream)
+        ctx.admm_solve(g, ip_d, im_d, cfg=cfg)
+        e1.record(stream)
+        e1.synchronize()
+        launches += ctx.launch_count()
+        tot += e0.elapsed_time(e1) / 1e3
+    c1 = ctx.admm_counters()
+    from paper_1607_00531_b200 import shard
+    tmax = shard.max_over_ranks(tot, dist, dev)
+    world = dist.get_world_size() if dist is not None else 1
+    ctx.profile(True)
+    ctx.profile_reset()
+    ctx.admm_solve(g, ip_d, im_d, cfg=cfg)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    bms, bn = prof.get("admm_bstep", (0.0, 0))
+    # line-search counters from the diagnostic instantiation (one solve)
+    from paper_1607_00531_b200.epicorr import Context
+    ctx.set_mode(0)
+    ctx.set_mode(Context.MODE_BSTEP_TIMING)
+    ctx.admm_solve(g, ip_d, im_d, cfg=cfg)
+    cnt = ctx.bstep_counters()
+    ctx.set_mode(0)
+    out = {"metric": f"voxel-iterations/s (ADMM x400, {'x'.join(map(str, g.dims()))}, fp64)",
+           "value": g.faces * iters * k * world / tmax, "unit": UNIT,
+           "time_to_solution_s": tmax / k, "steps": k, "gpu_launches": launches,
+           "bstep_ms_per_launch": bms / max(bn, 1),
+           "bstep_share": bms / max(1e-30, sum(v[0] for v in prof.values())),
+           "sqp_iterations_per_solve": (c1[2] - c0[2]) // k,
+           "qp_iterations_per_solve": (c1[3] - c0[3]) // k,
+           "line_search": {kk: cnt[kk] for kk in ("ls_searches", "ls_trials", "ls_undecided",
+                                                   "ls_failed", "acc0", "acc1", "acc2_3",
+                                                   "acc4_7", "acc8_15", "acc16_31", "acc32_39")},
+           "workload": f"ADMM {a.config} x400 intensity, {iters} iterations, fp64, from b=0"}
+    if rank == 0 and not a.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_windows_baseline(ctx, d, ip_d, im_d, iters,
+                                                       a.config + " x400",
+                                                       starts=[0, iters // 2], n=1)
         except Exception as e:
             out["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(e)[:120]}
     return out
@@ -475,9 +686,11 @@ def run_slabs(a, iters):
     cpu = None
     if rank == 0 and not a.no_cpu_baseline:
         try:
-            kind, dt, cores = cpu_reference(d, 1, os.cpu_count() or 1)
+            chk, kind, cores = ref_checker(os.cpu_count() or 1)
+            dt, _, _ = ref_admm_window(chk, cores, d, None, 1)
             cpu = {"value": g.faces / dt, "unit": UNIT, "cores": cores, "kind": kind,
-                   "sample": f"1 ADMM iteration of the full {a.config} volume"}
+                   "cpu_model": cpu_model(),
+                   "sample": f"ADMM iteration 1 of the full {a.config} volume"}
         except Exception as e:
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
                    "sample": str(e)[:120]}
@@ -687,20 +900,24 @@ def main():
                 "kernels": kernels}
 
     cpu = None
-    if rank == 0 and not a.no_cpu_baseline:
+    if rank == 0 and not a.no_cpu_baseline and a.config != "C4":
         try:
             one = synth.VolumePairData(g, np.ascontiguousarray(ipn[:g.cells]),
                                        np.ascontiguousarray(imn[:g.cells]), None)
-            kind, dt, cores = cpu_reference(one, a.ref_iters, os.cpu_count() or 1)
-            cpu = {"value": g.faces * a.ref_iters / dt, "unit": UNIT, "cores": cores, "kind": kind,
-                   "sample": f"{a.ref_iters} ADMM iterations of the {a.config} solve"}
+            cpu = cpu_windows_baseline(ctx, one, ip_d, im_d, iters, a.config,
+                                       starts=[int(iters * f) for f in (0, .2, .4, .6, .8)], n=2)
         except Exception as e:  # the checker is optional on a bench box
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
                    "sample": str(e)[:120]}
 
-    gn = None
+    gn = gn3 = x400 = None
     if not a.no_gn and a.config != "C4":
-        gn = run_gn_leg(a, ctx, dev, stream, flush, rank, dist)
+        gn = run_gn_leg(a, ctx, dev, stream, flush, rank, dist, a.gn_config, cpu_windows=10)
+        if a.config == "C3" and not a.no_gn_c3:
+            gn3 = run_gn_leg(a, ctx, dev, stream, flush, rank, dist, "C3", cpu_windows=1,
+                             min_solves=3)
+    if a.config == "C3" and not a.no_x400 and a.scale == 1.0:
+        x400 = run_x400_leg(a, ctx, dev, stream, flush, iters, rank, dist)
     f32 = None
     if not a.no_f32 and a.config != "C4":
         f32 = run_f32_leg(a, ctx, dev, stream, flush, g, ipn, imn, iters, last_b, dist)
@@ -710,20 +927,18 @@ def main():
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_max / a.steps * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"ADMM {a.config} {'x'.join(map(str, g.dims()))}, "
-                                       f"{iters} iterations, fp64, from b=0",
-                           "faces": g.faces, "iterations": iters, "intensity_scale": a.scale,
-                           "pairs": total_pairs,
-                           "parallelism": (f"pairs sharded {total_pairs}/{world} ranks"
-                                           if a.config == "C4" else f"replicas x{world}"),
-                           "l2": "256 MB flush write before every timed step; working set > L2",
-                           "time_to_solution_s": t_max / a.steps},
+                "config": admm_config_dict(a, g, iters),
+                "time_to_solution_s": t_max / a.steps,
                 "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 2 * nc * 8 * npairs,
                         "d2h_bytes_per_step": 3 * nf * 8 * npairs},
                 "gpu_launches": launches, "clocks": clk.summary(),
                 "roofline": roofline, "cpu_baseline": cpu}
         if gn is not None:
             line["gn"] = gn
+        if gn3 is not None:
+            line["gn_c3"] = gn3
+        if x400 is not None:
+            line["x400"] = x400
         if f32 is not None:
             line["fp32"] = f32
         print(json.dumps(line), flush=True)

@@ -162,10 +162,12 @@ enum {
     EPC_MODE_EXACT_SUMS = 1 << 14
 };
 int epc_set_mode(epc_context* ctx, int mode_bits);
-/* ADMM stop/rho decisions since the context was created: out2[0] taken on
- * certified enclosures of the reference's sequential sums, out2[1] on the
- * exact sequential sums (undecidable enclosure, or EPC_MODE_EXACT_SUMS). */
-int epc_decision_stats(epc_context* ctx, long long* out2);
+/* Cumulative ADMM counters of the context (epc_admm_solve / _batch):
+ * out4[0] stop/rho decisions taken on certified enclosures of the
+ * reference's sequential sums, out4[1] decisions taken on the exact
+ * sequential sums (undecidable enclosure, or EPC_MODE_EXACT_SUMS),
+ * out4[2] b-step SQP iterations, out4[3] QP iterations (BUpdateStats sums). */
+int epc_admm_counters(epc_context* ctx, long long* out4);
 /* Phase cycle totals of the b-step kernel since timing was enabled (lane 0
  * clock64 deltas): model, fval sums, factor, solves, QP rest, KKT, step
  * sums, line search, clamp+store, column fetch. */

@@ -34,7 +34,7 @@ EXPORTS = [
     "epc_multilevel_solve", "epc_avg_x1", "epc_diff_x1", "epc_diff_x1_adjoint",
     "epc_smoother_hessian_apply", "epc_tridiag_apply", "epc_tridiag_solve_batched", "epc_dct_apply",
     "epc_distance_hessian_apply", "epc_is_strictly_feasible", "epc_correct_pair", "epc_ssd", "epc_ncc", "epc_simulate_pair", "epc_write_volume", "epc_read_volume",
-    "epc_permute_to_axis1", "epc_unpermute_field", "epc_decision_stats", "epc_slab_seq_sums", "epc_slab_d1_norm_inf",
+    "epc_permute_to_axis1", "epc_unpermute_field", "epc_admm_counters", "epc_slab_seq_sums", "epc_slab_d1_norm_inf",
 ]
 
 
@@ -64,7 +64,7 @@ def _declare(L):
     L.epc_last_error.argtypes = [X]
     L.epc_last_error.restype = C.c_char_p
     L.epc_set_mode.argtypes = [X, C.c_int]
-    L.epc_decision_stats.argtypes = [X, C.POINTER(C.c_longlong)]
+    L.epc_admm_counters.argtypes = [X, C.POINTER(C.c_longlong)]
     L.epc_slab_seq_sums.argtypes = [X, C.c_longlong, X, X, X, X, dptr]
     L.epc_slab_d1_norm_inf.argtypes = [X, G, C.c_int, C.c_int, X, dptr]
     L.epc_profile_enable.argtypes = [X, C.c_int]

@@ -741,6 +741,8 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
                     --n_active;
                     continue;
                 }
+                ctx->sqp_total += ci[2];
+                ctx->qp_total += ci[3];
                 epc_admm_row row{};
                 row.level = level_tag;
                 row.iter = it;
@@ -1056,10 +1058,12 @@ void epc_profile_reset(epc_context* ctx) {
 
 long epc_launch_count(const epc_context* ctx) { return ctx->launches; }
 
-int epc_decision_stats(epc_context* ctx, long long* out2) {
-    if (!ctx || !out2) return EPC_ERR_INVALID_ARGUMENT;
-    out2[0] = ctx->dec_certified;
-    out2[1] = ctx->dec_exact;
+int epc_admm_counters(epc_context* ctx, long long* out4) {
+    if (!ctx || !out4) return EPC_ERR_INVALID_ARGUMENT;
+    out4[0] = ctx->dec_certified;
+    out4[1] = ctx->dec_exact;
+    out4[2] = ctx->sqp_total;
+    out4[3] = ctx->qp_total;
     return EPC_OK;
 }
 void epc_reset_launch_count(epc_context* ctx) { ctx->launches = 0; }

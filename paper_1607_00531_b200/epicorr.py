@@ -136,12 +136,12 @@ class Context:
     MODE_BSTEP_CHAINED = 1 << 13
     MODE_EXACT_SUMS = 1 << 14
 
-    def decision_stats(self):
-        """ADMM stop/rho decisions so far: (certified from the tree sums,
-        taken on the reference's exact sequential sums)."""
-        out = (C.c_longlong * 2)()
-        self._check(self.lib.epc_decision_stats(self.h, out))
-        return int(out[0]), int(out[1])
+    def admm_counters(self):
+        """Cumulative (decisions certified from the tree sums, decisions taken
+        on the reference's exact sequential sums, SQP iterations, QP iterations)."""
+        out = (C.c_longlong * 4)()
+        self._check(self.lib.epc_admm_counters(self.h, out))
+        return tuple(int(x) for x in out)
 
     def bstep_counters(self):
         out = (C.c_longlong * 18)()

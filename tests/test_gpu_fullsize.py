@@ -60,9 +60,9 @@ def test_admm_c3_full_trajectory_bitwise_vs_reference(ctx):
     r = ref.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
     rhos = [x["rho"] for x in r["rows"]]
     assert len(set(rhos)) > 5  # the trajectory does walk rho (the window the test is for)
-    c0 = ctx.decision_stats()
+    c0 = ctx.admm_counters()
     o = ctx.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
-    c1 = ctx.decision_stats()
+    c1 = ctx.admm_counters()
     _check_admm(o, r)
     assert (c1[0] - c0[0]) + (c1[1] - c0[1]) == 100
     try:
@@ -71,7 +71,7 @@ def test_admm_c3_full_trajectory_bitwise_vs_reference(ctx):
     finally:
         ctx.set_mode(0)
     _check_admm(e, r, rows_exact=True)
-    c2 = ctx.decision_stats()
+    c2 = ctx.admm_counters()
     assert c2[1] - c1[1] == 100
 
 
@@ -174,16 +174,16 @@ def test_exact_sums_mode_rows_bitwise_c1(ctx, oracle):
     d = synth.make_config("C1")
     cfg = abi.AdmmConfig(max_iter=50, **EXACT)
     r = oracle.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
-    c0 = ctx.decision_stats()
+    c0 = ctx.admm_counters()
     try:
         ctx.set_mode(Context.MODE_EXACT_SUMS)
         o = ctx.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
     finally:
         ctx.set_mode(0)
-    c1 = ctx.decision_stats()
+    c1 = ctx.admm_counters()
     assert c1[1] - c0[1] == 50
     _check_admm(o, r, rows_exact=True)
     o2 = ctx.admm_solve(d.grid, d.iplus, d.iminus, cfg=cfg)
-    c2 = ctx.decision_stats()
+    c2 = ctx.admm_counters()
     assert c2[0] - c1[0] == 50  # all certified at C1 (no near-tie)
     _check_admm(o2, r)
