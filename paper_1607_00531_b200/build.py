@@ -27,7 +27,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-prec-div=true", "-pr
 
 # the fp32 variant has no bitwise contract: contraction to FMA is allowed there
 FMAD_ON = {"admm_f32.cu"}
-LIBS = ["-lcudart", "-lcublas"]
+LIBS = ["-lcudart"]
 
 
 def _stale(target, deps):

@@ -736,19 +736,7 @@ __global__ void k_reduce_f32cols(const float* kkt, const double* sr, const doubl
     }
 }
 
-// rhs = rho V (b + u)
-__global__ void k_rhs_f32(const float* b, const float* u, float w, float* out, long long n) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        out[i] = w * (b[i] + u[i]);
-}
 
-// spectral divide (operators.cpp:404-410): face f of column c = f / n1
-__global__ void k_div_f32(float* x, const float* lam23, float aV, float rV, int n1, long long n) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        x[i] = x[i] / (aV * lam23[i / n1] + rV);
-}
 
 // dual update + residual / Lagrangian partial sums (admm.cpp:453-476,
 // 287-299): u_new = u + b - z; per block {sum (b-z)^2, sum (zo-z)^2,
@@ -820,14 +808,6 @@ void launch_reduce_f32cols(epc_context* ctx, const BStepF32Params& P, long long 
     EPC_LAUNCH(ctx, "reduce_f32cols", k_reduce_f32cols, 1, 512, 0, P.col_kkt, P.col_sr, P.col_sd,
                P.col_err, P.col_work, ncol, od, oi);
 }
-void launch_rhs_f32(epc_context* ctx, int blocks, const float* b, const float* u, float w, float* out,
-                    long long n) {
-    EPC_LAUNCH(ctx, "rhs_f32", k_rhs_f32, blocks, 256, 0, b, u, w, out, n);
-}
-void launch_div_f32(epc_context* ctx, int blocks, float* x, const float* lam23, float aV, float rV,
-                    int n1, long long n) {
-    EPC_LAUNCH(ctx, "div_f32", k_div_f32, blocks, 256, 0, x, lam23, aV, rV, n1, n);
-}
 void launch_dual_f32(epc_context* ctx, int blocks, const float* b, const float* z, const float* zo,
                      const float* u, float* un, int n1, int m2, int m3, float ih2, float ih3,
                      long long n, double* part) {
@@ -839,4 +819,119 @@ void launch_scale_f32(epc_context* ctx, int blocks, float* x, float a, long long
 }
 void launch_d2f(epc_context* ctx, int blocks, const double* a, float* b, long long n) {
     EPC_LAUNCH(ctx, "d2f", k_d2f, blocks, 256, 0, a, b, n);
+}
+
+// ---------------------------------------------------------------------------
+// fp32 z-step transforms: the dense DCT-II products of DctCoupledSolver
+// (operators.cpp:347-418) as one hand-written FFMA GEMM, out = C * in along
+// axis 2 or 3, with the rhs formation rho V (b + u) fused into the operand
+// load and the spectral divide into the epilogue (the fp32 variant has no
+// bitwise contract: contraction to FMA is on, k ascending).
+//
+// C is M x K row-major (the DCT matrix or its transpose); the data operand
+// element (k, n) sits at k * kstride + (n / cdiv) * cstride + n % cdiv, so
+// one kernel serves both axes (axis 2: k = j, n = i + n1 k3; axis 3: k = k3,
+// n = i + n1 j). Tile BM = 16 RM rows x 128 columns per 256-thread CTA,
+// 16-deep K slabs double-buffered through registers, each thread an RM x 8
+// strided microtile (conflict-free shared reads).
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int F32_BN = 128, F32_BK = 16, F32_NT = 256;
+}
+
+template <int PRO, int EPI, int RM>
+__global__ void __launch_bounds__(F32_NT) k_dct_gemm_f32(DctGemmF32 p) {
+    constexpr int BM = 16 * RM;
+    __shared__ float As[F32_BK][BM + 4];
+    __shared__ float Bs[F32_BK][F32_BN];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int row0 = blockIdx.y * BM;
+    const long long col0 = (long long)blockIdx.x * F32_BN;
+    // B loads: column ln fixed, rows lk + 2 t
+    const int ln = tid & (F32_BN - 1), lk = tid >> 7;
+    const long long lcol = col0 + ln;
+    const bool lok = lcol < p.N;
+    const long long lmap = lok ? (lcol / p.cdiv) * p.cstride + (lcol % p.cdiv) : 0;
+    // A loads: (am + 16 t, ak)
+    const int am = tid >> 4, ak = tid & 15;
+    constexpr int NA = RM, NB = F32_BK / 2;
+    float acc[RM][8];
+#pragma unroll
+    for (int r = 0; r < RM; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[r][c] = 0.0f;
+    float ra[NA], rb[NB];
+    auto load = [&](int k0) {
+#pragma unroll
+        for (int t = 0; t < NA; ++t) {
+            const int m = row0 + am + 16 * t, k = k0 + ak;
+            ra[t] = (m < p.M && k < p.K) ? __ldg(p.A + (size_t)m * p.K + k) : 0.0f;
+        }
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+            const int k = k0 + lk + 2 * t;
+            float v = 0.0f;
+            if (lok && k < p.K) {
+                const long long a = (long long)k * p.kstride + lmap;
+                v = PRO == PRO_RHS ? p.w * (__ldg(p.in0 + a) + __ldg(p.in1 + a)) : __ldg(p.in0 + a);
+            }
+            rb[t] = v;
+        }
+    };
+    load(0);
+    for (int k0 = 0; k0 < p.K; k0 += F32_BK) {
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < NA; ++t) As[ak][am + 16 * t] = ra[t];
+#pragma unroll
+        for (int t = 0; t < NB; ++t) Bs[lk + 2 * t][ln] = rb[t];
+        __syncthreads();
+        if (k0 + F32_BK < p.K) load(k0 + F32_BK);
+#pragma unroll
+        for (int kk = 0; kk < F32_BK; ++kk) {
+            float a[RM], b[8];
+#pragma unroll
+            for (int r = 0; r < RM; ++r) a[r] = As[kk][ty + 16 * r];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) b[c] = Bs[kk][tx + 16 * c];
+#pragma unroll
+            for (int r = 0; r < RM; ++r)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const long long col = col0 + tx + 16 * c;
+        if (col >= p.N) continue;
+        const long long cmap = (col / p.cdiv) * p.cstride + (col % p.cdiv);
+#pragma unroll
+        for (int r = 0; r < RM; ++r) {
+            const int row = row0 + ty + 16 * r;
+            if (row >= p.M) continue;
+            const long long f = (long long)row * p.kstride + cmap;
+            float v = acc[r][c];
+            if (EPI == EPI_DIVIDE) v = v / (p.aV * p.lam23[f / p.n1] + p.rV);
+            p.out[f] = v;
+        }
+    }
+}
+
+void launch_dct_gemm_f32(epc_context* ctx, const char* name, const DctGemmF32& p, int pro, int epi) {
+    const bool t96 = p.M % 96 == 0;
+    const int bm = t96 ? 96 : 64;
+    dim3 grid((unsigned)((p.N + F32_BN - 1) / F32_BN), (unsigned)((p.M + bm - 1) / bm));
+#define F32_GEMM(PRO, EPI)                                                                  \
+    if (t96) EPC_LAUNCH(ctx, name, (k_dct_gemm_f32<PRO, EPI, 6>), grid, F32_NT, 0, p);      \
+    else EPC_LAUNCH(ctx, name, (k_dct_gemm_f32<PRO, EPI, 4>), grid, F32_NT, 0, p);
+    if (pro == PRO_RHS && epi == EPI_DIVIDE) {
+        F32_GEMM(PRO_RHS, EPI_DIVIDE)
+    } else if (pro == PRO_RHS) {
+        F32_GEMM(PRO_RHS, EPI_STORE)
+    } else if (epi == EPI_DIVIDE) {
+        F32_GEMM(PRO_PLAIN, EPI_DIVIDE)
+    } else {
+        F32_GEMM(PRO_PLAIN, EPI_STORE)
+    }
+#undef F32_GEMM
 }

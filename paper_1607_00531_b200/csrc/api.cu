@@ -13,7 +13,6 @@
 #include <string>
 #include <vector>
 
-#include <cublas_v2.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -441,6 +440,11 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
     P.cert = (ctx->mode & EPC_MODE_BSTEP_CHAINED) ? 0 : 1;
     if (tail && total < (1LL << 31)) P.col_ns = slot_t<unsigned>(ctx, S_CTIME, (size_t)total);
     P.cta_span = tail ? slot_t<unsigned long long>(ctx, S_GN8, (size_t)slots * 2) : nullptr;
+    static const char* dump = getenv("EPC_BSTEP_DUMP");  // dev aid: per-column records
+    if (tail && dump) {
+        P.col_sn = slot_t<float>(ctx, S_GN7, (size_t)total * 2);
+        CK(cudaMemsetAsync(P.col_sn, 0, (size_t)total * 8, ctx->stream));
+    }
     EPC_LAUNCH(ctx, "admm_bstep", kern, (unsigned)slots, 32, smem, P);
     if (tail) {
         std::vector<unsigned long long> t((size_t)slots * 2);
@@ -474,6 +478,24 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
                              ci[2 * total + c], ci[3 * total + c]);
             }
             std::fprintf(stderr, "\n");
+            static long long launch_no = 0;
+            static const int every = getenv("EPC_BSTEP_DUMP_EVERY") ? atoi(getenv("EPC_BSTEP_DUMP_EVERY")) : 1;
+            const bool keep = every <= 1 || (launch_no % every) == 0 || (launch_no % every) == every - 1;
+            ++launch_no;
+            if (dump && P.col_sn && keep) {  // ns, sqp, qp, sn0, sn1 per column, per kept launch
+                std::vector<float> sn((size_t)total * 2);
+                CK(cudaMemcpyAsync(sn.data(), P.col_sn, total * 8, cudaMemcpyDeviceToHost, ctx->stream));
+                sync(ctx);
+                if (FILE* f = std::fopen(dump, "ab")) {
+                    const long long t = total;
+                    std::fwrite(&t, 8, 1, f);
+                    std::fwrite(ns.data(), 4, total, f);
+                    std::fwrite(ci.data() + total, 4, total, f);
+                    std::fwrite(ci.data() + 2 * total, 4, total, f);
+                    std::fwrite(sn.data(), 4, 2 * total, f);
+                    std::fclose(f);
+                }
+            }
             static std::vector<unsigned> prev;
             if (prev.size() == ns.size()) {
                 long long heavy = 0, was = 0;
@@ -984,7 +1006,6 @@ void epc_context_destroy(epc_context* ctx) {
         cudaEventDestroy(pe.stop);
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
-    if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

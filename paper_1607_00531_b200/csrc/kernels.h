@@ -30,6 +30,7 @@ struct BStepParams {
     int cert;           // 1: decide SQP / line-search tests on certified enclosures
     unsigned long long* cta_span;  // optional [2 x grid]: %globaltimer at CTA start / exit (dev aid)
     unsigned* col_ns;   // optional: each column's duration in ns (dev aid, EPC_BSTEP_TAIL)
+    float* col_sn;      // optional [2 x total]: step norms of SQP iterations 0, 1 (dev aid)
 };
 // DH = HPow2 | HGen (model.cuh); DIAG: phase timing / counters and the
 // chained mode compiled in (diagnostic instantiation, selected by ctx->mode)
@@ -193,13 +194,16 @@ struct PcgUpdArgs {
     long long ncol;
     double* partials;
     int tile_rs;  // k_pcg_update_bj: shared-memory row stride (odd, >= n1)
+    int seg;      // block-Jacobi sweeps: segment length of the warp-per-column chains
+                  // (5, 9 or 17; three staged arrays), 0 = thread-per-column chains
 };
 __global__ void k_pcg_start(const double* g, double* r, double* d, long long n, double* partials,
                             PcgState* S);
 __global__ void k_pcg_hvp(PcgHvArgs A, PcgState* S);
-void launch_pcg_update_bj(epc_context* ctx, int cpw, int blocks, size_t smem, const PcgUpdArgs& U,
+void launch_pcg_update_bj(epc_context* ctx, int cpw, int seg, int blocks, size_t smem, const PcgUpdArgs& U,
                           PcgState* S);
-void set_pcg_update_bj_smem(int cpw, int bytes);
+void set_pcg_update_bj_smem(int cpw, int seg, int bytes);
+bool pcg_variant_ok(int cpw, int seg);  // an instantiated (columns per block, segment) pair
 struct PcgLoopArgs {
     PcgHvArgs H;
     PcgUpdArgs U;
@@ -208,7 +212,8 @@ struct PcgLoopArgs {
     size_t part_cap;           // doubles available in each partials buffer
     unsigned* bar;             // grid barrier counter, zeroed before the launch
 };
-bool launch_pcg_loop(epc_context* ctx, int cpw, size_t smem, const PcgLoopArgs& L, PcgState* S);
+bool launch_pcg_loop(epc_context* ctx, int cpw, int seg, size_t smem, const PcgLoopArgs& L,
+                     PcgState* S);
 __global__ void k_vec_differs(const double* a, const double* b, long long n, int* flag);
 __global__ void k_first_error(const int* col_err, long long ncol, int* out);
 __global__ void k_pcg_update(PcgUpdArgs A, PcgState* S);
@@ -275,14 +280,26 @@ int bstep_f32_slots_per_sm(size_t smem);
 void launch_bstep_f32(epc_context* ctx, int slots, size_t smem, const BStepF32Params& P);
 void launch_reduce_f32cols(epc_context* ctx, const BStepF32Params& P, long long ncol, double* od,
                            long long* oi);
-void launch_rhs_f32(epc_context* ctx, int blocks, const float* b, const float* u, float w, float* out,
-                    long long n);
-void launch_div_f32(epc_context* ctx, int blocks, float* x, const float* lam23, float aV, float rV,
-                    int n1, long long n);
 void launch_dual_f32(epc_context* ctx, int blocks, const float* b, const float* z, const float* zo,
                      const float* u, float* un, int n1, int m2, int m3, float ih2, float ih3,
                      long long n, double* part);
 void launch_scale_f32(epc_context* ctx, int blocks, float* x, float a, long long n);
+// fp32 DCT GEMM (admm_f32.cu): out = A (M x K) * data along one axis; the data
+// element (k, n) sits at k*kstride + (n/cdiv)*cstride + n%cdiv. PRO_RHS forms
+// w (in0 + in1) on load; EPI_DIVIDE divides by aV lam23[f / n1] + rV.
+struct DctGemmF32 {
+    const float* A;
+    int M, K;
+    long long N;
+    const float *in0, *in1;
+    float w;
+    long long kstride, cdiv, cstride;
+    float* out;
+    const float* lam23;
+    float aV, rV;
+    int n1;
+};
+void launch_dct_gemm_f32(epc_context* ctx, const char* name, const DctGemmF32& p, int pro, int epi);
 void launch_d2f(epc_context* ctx, int blocks, const double* a, float* b, long long n);
 
 // ---- the reference's test-side helpers (operators_t2.cu) ----

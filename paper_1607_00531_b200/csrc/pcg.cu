@@ -365,16 +365,153 @@ __global__ void __launch_bounds__(256) k_pcg_hvp(PcgHvArgs A, PcgState* S) {
 // of odd stride RS so the per-thread sweeps are bank-conflict free):
 //   1. all threads: coalesced flat pass over the span, element-wise updates
 //      of d and r (written back), r and l staged;
-//   2. thread cc < CPW: forward sweep v_i = r_i - l_{i-1} v_{i-1};
+//   2. forward sweep v_i = r_i - l_{i-1} v_{i-1}: a warp per column as a
+//      segmented chain (sweeps_seg, into a third staged array T), or thread
+//      cc < CPW as the plain chain (sweeps_thread; seg = 0);
 //   3. all threads: v_i / d_i (d read coalesced from the factor);
-//   4. thread cc: backward sweep w_i = v_i - l_i w_{i+1};
+//   4. backward sweep w_i = v_i - l_i w_{i+1}, the same way;
 //   5. all threads: z written coalesced, partial r.z.
 // The sweeps do the operations of ldlt_solve_warp in the same order, so z
 // is bitwise the same; every global access is a flat coalesced pass.
 constexpr int PCG_NT = 256;
 
-// One column group (steps 1-5 above) for the block; accumulates r.r, r.z.
-// COH: p and q come from other blocks of the same persistent kernel.
+// TridiagFactor::solve_in_place (operators.cpp:248-262) on the staged group:
+// forward sweep x[i] -= l[i-1] x[i-1], the divisions by d, backward sweep
+// x[i] -= l[i] x[i+1]. Thread-per-column form (the reference's chains as
+// written): CPW of the block's threads run the sweeps.
+template <class SIDX>
+__device__ __forceinline__ void sweeps_thread(const PcgUpdArgs& A, int nc, double* X,
+                                              const double* Y, size_t base, const SIDX& sidx,
+                                              int ne, int ne2) {
+    const int tid = threadIdx.x, n1 = A.n1, RS = A.tile_rs;
+    const double* __restrict__ FD = A.fd;
+    if (tid < nc) {
+        double* x = X + tid * RS;
+        const double* y = Y + tid * RS;
+        double prev = x[0];
+#pragma unroll 4
+        for (int i = 1; i < n1; ++i) {
+            prev = x[i] - y[i - 1] * prev;
+            x[i] = prev;
+        }
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int h = tid; h < ne2; h += PCG_NT) {
+        const double2 dd = __ldg(reinterpret_cast<const double2*>(FD + base + 2 * (size_t)h));
+        const int k0 = sidx(2 * h), k1 = sidx(2 * h + 1);
+        X[k0] = X[k0] / dd.x;
+        X[k1] = X[k1] / dd.y;
+    }
+    if ((ne & 1) && tid == 0) {
+        const int k = sidx(ne - 1);
+        X[k] = X[k] / __ldg(FD + base + ne - 1);
+    }
+    __syncthreads();
+    if (tid < nc) {
+        double* x = X + tid * RS;
+        const double* y = Y + tid * RS;
+        double nxt = x[n1 - 1];
+#pragma unroll 4
+        for (int i = n1 - 2; i >= 0; --i) {
+            nxt = x[i] - y[i] * nxt;
+            x[i] = nxt;
+        }
+    }
+    __syncthreads();
+}
+
+// Segmented form of the same sweeps, bitwise: one warp per column, each lane
+// a segment of S steps started from a guess, repeated until every lane's
+// start equals its predecessor's end bit for bit (then, by induction from
+// lane 0's exact start, every stored value is the one-thread chain's: same
+// operations on the same operands). The block-Jacobi factor has |l| well
+// below 1 (the alpha V Laplacian plus the cross-column diagonal dominate),
+// so a wrong start is forgotten within a few segments: 3-4 rounds of S
+// steps instead of n1 - 1. Out of place (X -> T forward, T -> X backward) so
+// a lane's guess is never overwritten under it; after SEG_ROUNDS rounds lane
+// 0 runs the one-thread chain instead.
+constexpr int PCG_SEG_ROUNDS = 8;
+template <int S, bool BWD>
+__device__ __forceinline__ bool pcg_seg_sweep(const double* __restrict__ src,
+                                              double* __restrict__ dst,
+                                              const double* __restrict__ l, int n) {
+    const int lane = threadIdx.x & 31;
+    const int r0 = 1 + lane * S;
+    const int cnt = max(0, min(S, n - r0));
+    if (lane == 0) dst[BWD ? n - 1 : 0] = src[BWD ? n - 1 : 0];
+    double st = src[BWD ? n - min(r0, n) : min(r0, n) - 1];
+    // rolled (the loop kernel runs at a 64-register cap); lanes past the end
+    // (cnt < S) only repeat their last valid element
+    const int e0 = BWD ? n - 1 - min(r0, n - 1) : min(r0, n - 1);
+    for (int round = 0; round < PCG_SEG_ROUNDS; ++round) {
+        double p = st;
+        int e = e0;
+#pragma unroll 1
+        for (int j = 0; j < cnt; ++j, e += BWD ? -1 : 1) {
+            p = src[e] - l[BWD ? e : e - 1] * p;
+            dst[e] = p;
+        }
+        const double end = cnt > 0 ? p : st;
+        const double pe = __shfl_up_sync(FULL_MASK, end, 1);
+        const bool ok = lane == 0 || cnt == 0 ||
+                        __double_as_longlong(pe) == __double_as_longlong(st);
+        if (__all_sync(FULL_MASK, ok)) return true;
+        if (lane > 0) st = pe;
+    }
+    return false;
+}
+
+template <int S, int CPW, class SIDX>
+__device__ __forceinline__ void sweeps_seg(const PcgUpdArgs& A, int nc, double* X, const double* Y,
+                                           size_t base, const SIDX& sidx, int ne, int ne2) {
+    const int tid = threadIdx.x, lane = tid & 31, n1 = A.n1, RS = A.tile_rs;
+    double* const T = const_cast<double*>(Y) + CPW * RS;  // third staged array
+    const double* __restrict__ FD = A.fd;
+    for (int cc = tid >> 5; cc < nc; cc += PCG_NT / 32) {
+        const double* x = X + cc * RS;
+        double* t = T + cc * RS;
+        const double* y = Y + cc * RS;
+        if (!pcg_seg_sweep<S, false>(x, t, y, n1) && lane == 0) {
+            double prev = x[0];
+            t[0] = prev;
+            for (int i = 1; i < n1; ++i) {
+                prev = x[i] - y[i - 1] * prev;
+                t[i] = prev;
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int h = tid; h < ne2; h += PCG_NT) {
+        const double2 dd = __ldg(reinterpret_cast<const double2*>(FD + base + 2 * (size_t)h));
+        const int k0 = sidx(2 * h), k1 = sidx(2 * h + 1);
+        T[k0] = T[k0] / dd.x;
+        T[k1] = T[k1] / dd.y;
+    }
+    if ((ne & 1) && tid == 0) {
+        const int k = sidx(ne - 1);
+        T[k] = T[k] / __ldg(FD + base + ne - 1);
+    }
+    __syncthreads();
+    for (int cc = tid >> 5; cc < nc; cc += PCG_NT / 32) {
+        double* x = X + cc * RS;
+        const double* t = T + cc * RS;
+        const double* y = Y + cc * RS;
+        if (!pcg_seg_sweep<S, true>(t, x, y, n1) && lane == 0) {
+            double nxt = t[n1 - 1];
+            x[n1 - 1] = nxt;
+            for (int i = n1 - 2; i >= 0; --i) {
+                nxt = t[i] - y[i] * nxt;
+                x[i] = nxt;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// 16-byte load; COH: written by other blocks of the same persistent kernel
+// (read through L2, not the incoherent L1 path).
 template <bool COH>
 __device__ __forceinline__ double2 ld_vec2(const double* p) {
     return COH ? __ldcg(reinterpret_cast<const double2*>(p)) : __ldg(reinterpret_cast<const double2*>(p));
@@ -385,7 +522,7 @@ __device__ __forceinline__ double2 ld_vec2(const double* p) {
 // flat passes move two faces per thread (16-byte accesses): a group starts
 // at face c0 n1 with c0 a multiple of CPW (even), and the span nc n1 is even
 // unless nc is odd (the last group), whose final face goes scalar.
-template <int CPW, bool UPD, bool COH>
+template <int CPW, bool UPD, bool COH, int SEG>
 __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long long gi, double* X,
                                          double* Y, double& rr, double& rz) {
     const int tid = threadIdx.x;
@@ -444,40 +581,8 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
         stage1(ne - 1, r, __ldg(FL + o));
     }
     __syncthreads();
-    if (tid < nc) {
-        double* x = X + tid * RS;
-        const double* y = Y + tid * RS;
-        double prev = x[0];
-#pragma unroll 4
-        for (int i = 1; i < n1; ++i) {
-            prev = x[i] - y[i - 1] * prev;
-            x[i] = prev;
-        }
-    }
-    __syncthreads();
-#pragma unroll 2
-    for (int h = tid; h < ne2; h += PCG_NT) {
-        const double2 dd = __ldg(reinterpret_cast<const double2*>(FD + base + 2 * (size_t)h));
-        const int k0 = sidx(2 * h), k1 = sidx(2 * h + 1);
-        X[k0] = X[k0] / dd.x;
-        X[k1] = X[k1] / dd.y;
-    }
-    if ((ne & 1) && tid == 0) {
-        const int k = sidx(ne - 1);
-        X[k] = X[k] / __ldg(FD + base + ne - 1);
-    }
-    __syncthreads();
-    if (tid < nc) {
-        double* x = X + tid * RS;
-        const double* y = Y + tid * RS;
-        double nxt = x[n1 - 1];
-#pragma unroll 4
-        for (int i = n1 - 2; i >= 0; --i) {
-            nxt = x[i] - y[i] * nxt;
-            x[i] = nxt;
-        }
-    }
-    __syncthreads();
+    if (SEG) sweeps_seg<SEG, CPW>(A, nc, X, Y, base, sidx, ne, ne2);
+    else sweeps_thread(A, nc, X, Y, base, sidx, ne, ne2);
 #pragma unroll 2
     for (int h = tid; h < ne2; h += PCG_NT) {
         const size_t o = base + 2 * (size_t)h;
@@ -496,7 +601,7 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
     __syncthreads();
 }
 
-template <int CPW, bool UPD>
+template <int CPW, bool UPD, int SEG>
 __global__ void __launch_bounds__(PCG_NT) k_pcg_update_bj(PcgUpdArgs A, PcgState* S) {
     extern __shared__ __align__(16) double usm[];
     __shared__ double sh[8];
@@ -507,7 +612,7 @@ __global__ void __launch_bounds__(PCG_NT) k_pcg_update_bj(PcgUpdArgs A, PcgState
     const long long ngroups = (A.ncol + CPW - 1) / CPW;
     double rr = 0.0, rz = 0.0;
     for (long long gi = blockIdx.x; gi < ngroups; gi += gridDim.x)
-        bj_group<CPW, UPD, false>(A, a, gi, X, Y, rr, rz);
+        bj_group<CPW, UPD, false, SEG>(A, a, gi, X, Y, rr, rz);
     const double srr_b = block_sum(rr, sh);
     __syncthreads();
     const double srz_b = block_sum(rz, sh);
@@ -571,7 +676,7 @@ __device__ double block_fixed_sum(const double* part, int n, int stride, int off
     return out;
 }
 
-template <int CPW>
+template <int CPW, int SEG>
 #ifndef EPC_PCG_LOOP_MINB
 #define EPC_PCG_LOOP_MINB 4  // 64 registers: 4 resident blocks per SM (C2 GN solve 29.4 -> 23.0 ms; 5 spills)
 #endif
@@ -610,7 +715,7 @@ __global__ void __launch_bounds__(PCG_NT, EPC_PCG_LOOP_MINB) k_pcg_loop(PcgLoopA
         U.p = H.p_new;
         double rr = 0.0, rzp = 0.0;
         for (long long gi = blockIdx.x; gi < ngroups; gi += gridDim.x)
-            bj_group<CPW, true, true>(U, alpha, gi, X, Y, rr, rzp);
+            bj_group<CPW, true, true, SEG>(U, alpha, gi, X, Y, rr, rzp);
         const double srr_b = block_sum(rr, sh);
         __syncthreads();
         const double srz_b = block_sum(rzp, sh);
@@ -650,8 +755,23 @@ __global__ void __launch_bounds__(PCG_NT, EPC_PCG_LOOP_MINB) k_pcg_loop(PcgLoopA
 }
 
 // Cooperative launch of the loop; false when the device cannot hold the grid.
-bool launch_pcg_loop(epc_context* ctx, int cpw, size_t smem, const PcgLoopArgs& L, PcgState* S) {
-    const void* fn = cpw == 8 ? (const void*)k_pcg_loop<8> : (const void*)k_pcg_loop<16>;
+// (CPW, SEG) instantiations: 16 columns per block only for n1 <= ~160
+// (segment 5 covers them), 8 for longer columns (segments 9, 17)
+#define PCG_VARIANTS(X) X(16, 0) X(16, 5) X(8, 0) X(8, 9) X(8, 17)
+
+static const void* pcg_loop_fn(int cpw, int seg) {
+#define PCG_PICK(C, S) if (cpw == C && seg == S) return (const void*)k_pcg_loop<C, S>;
+    PCG_VARIANTS(PCG_PICK)
+#undef PCG_PICK
+    return nullptr;
+}
+
+bool pcg_variant_ok(int cpw, int seg) { return pcg_loop_fn(cpw, seg) != nullptr; }
+
+bool launch_pcg_loop(epc_context* ctx, int cpw, int seg, size_t smem, const PcgLoopArgs& L,
+                     PcgState* S) {
+    const void* fn = pcg_loop_fn(cpw, seg);
+    if (!fn) return false;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return false;
     int per_sm = 0;
@@ -673,25 +793,26 @@ bool launch_pcg_loop(epc_context* ctx, int cpw, size_t smem, const PcgLoopArgs& 
     return e == cudaSuccess;
 }
 
-void launch_pcg_update_bj(epc_context* ctx, int cpw, int blocks, size_t smem, const PcgUpdArgs& U,
-                          PcgState* S) {
+void launch_pcg_update_bj(epc_context* ctx, int cpw, int seg, int blocks, size_t smem,
+                          const PcgUpdArgs& U, PcgState* S) {
     const bool upd = U.phase == 1;
-    if (cpw == 8) {
-        if (upd) EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<8, true>), blocks, PCG_NT, smem, U, S);
-        else EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<8, false>), blocks, PCG_NT, smem, U, S);
-    } else {
-        if (upd) EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<16, true>), blocks, PCG_NT, smem, U, S);
-        else EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<16, false>), blocks, PCG_NT, smem, U, S);
+#define PCG_LAUNCH_UPD(C, SG)                                                                       \
+    if (cpw == C && seg == SG) {                                                                   \
+        if (upd) EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<C, true, SG>), blocks, PCG_NT, smem, U, S); \
+        else EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<C, false, SG>), blocks, PCG_NT, smem, U, S); \
+        return;                                                                                    \
     }
+    PCG_VARIANTS(PCG_LAUNCH_UPD)
+#undef PCG_LAUNCH_UPD
 }
 
-void set_pcg_update_bj_smem(int cpw, int bytes) {
+void set_pcg_update_bj_smem(int cpw, int seg, int bytes) {
     const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    if (cpw == 8) {
-        cudaFuncSetAttribute(k_pcg_update_bj<8, true>, attr, bytes);
-        cudaFuncSetAttribute(k_pcg_update_bj<8, false>, attr, bytes);
-    } else {
-        cudaFuncSetAttribute(k_pcg_update_bj<16, true>, attr, bytes);
-        cudaFuncSetAttribute(k_pcg_update_bj<16, false>, attr, bytes);
+#define PCG_SET_SMEM(C, SG)                                                     \
+    if (cpw == C && seg == SG) {                                               \
+        cudaFuncSetAttribute(k_pcg_update_bj<C, true, SG>, attr, bytes);        \
+        cudaFuncSetAttribute(k_pcg_update_bj<C, false, SG>, attr, bytes);       \
     }
+    PCG_VARIANTS(PCG_SET_SMEM)
+#undef PCG_SET_SMEM
 }

@@ -11,10 +11,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--outer", type=int, default=10)
+ap.add_argument("--ncu", action="store_true",
+                help="one GN step only, no warm-up (for ncu -k regex:pcg_loop -c 1)")
 a = ap.parse_args()
 d = synth.make_config(a.config, scale=a.scale)
 ctx = Context(0)
 cfg = abi.GnConfig(eta=1e-2, max_pcg=50, max_outer=a.outer)
+if a.ncu:
+    r = ctx.gn_solve(d.grid, d.iplus, d.iminus, cfg=abi.GnConfig(eta=1e-2, max_pcg=50, max_outer=1))
+    print("pcg_iters", r["rows"][1]["pcg_iters"], "faces", d.grid.faces)
+    sys.exit(0)
 ctx.gn_solve(d.grid, d.iplus, d.iminus, cfg=abi.GnConfig(eta=1e-2, max_pcg=5, max_outer=1))
 ctx.profile(True)
 ctx.profile_reset()

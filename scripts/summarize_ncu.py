@@ -67,5 +67,29 @@ def capture(src, dst):
     json.dump(d, open(dst, "w"), indent=1)
 
 
+def pcg(src, dst, pcg_iters, faces):
+    """capture of one k_pcg_loop launch (one PCG solve of pcg_iters
+    iterations): adds DRAM bytes per PCG iteration against the algorithmic
+    120 B/face per iteration."""
+    capture(src, dst)
+    d = json.load(open(dst))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = sum(float(d[k][0].replace(",", "")) * scale[d[k][1]]
+              for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    tu = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
+    t = float(d["gpu__time_duration.sum"][0].replace(",", "")) * tu[d["gpu__time_duration.sum"][1]]
+    n, f = int(pcg_iters), int(faces)
+    d["pcg_iterations"] = n
+    d["faces"] = f
+    d["dram_bytes_per_pcg_iteration"] = tot / n
+    d["alg_bytes_per_pcg_iteration"] = 120 * f
+    d["traffic_over_alg"] = tot / n / (120 * f)
+    d["dram_gbs_under_ncu"] = tot / t / 1e9
+    json.dump(d, open(dst, "w"), indent=1)
+
+
 if __name__ == "__main__":
-    {"launches": launches, "capture": capture}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    if sys.argv[1] == "pcg":
+        pcg(*sys.argv[2:6])
+    else:
+        {"launches": launches, "capture": capture}[sys.argv[1]](sys.argv[2], sys.argv[3])

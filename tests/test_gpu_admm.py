@@ -237,3 +237,33 @@ def test_b_update_segmented_chains_bitwise(ctx, oracle, alpha, rho):
         assert np.array_equal(out["b"], ref["b"]), (m, np.abs(out["b"] - ref["b"]).max())
         assert out["sqp_iters"] == ref["sqp_iters"] and out["qp_iters"] == ref["qp_iters"]
         assert out["kkt_violation"] == ref["kkt_violation"]
+
+
+@pytest.mark.parametrize("n,amp", [(60, 40.0), (200, 60.0), (257, 200.0)])
+def test_qp_large_active_sets_bitwise(ctx, oracle, n, amp):
+    """QPs whose active sets grow to tens of rows (as the x400 columns' do),
+    so the Schur systems are solved by the whole warp (warp_spd_solve: the
+    right-looking Cholesky whose every entry keeps the reference's ascending-k
+    chain) and p = w + sum_r lambda_r q_r runs four chains per lane: x,
+    lambda, signs, iteration counts and the KKT value bitwise vs the oracle."""
+    rng = np.random.default_rng(n)
+    nqp, h = 12, 1.0
+    gd = 3.0 + rng.uniform(0, 1, (nqp, n))
+    go = np.zeros((nqp, n))
+    go[:, :-1] = -1.0 + 0.2 * rng.uniform(-1, 1, (nqp, n - 1))
+    c = amp * np.cumsum(rng.uniform(-1, 1, (nqp, n)), axis=1) / np.sqrt(n)
+    x0 = np.zeros((nqp, n))
+    out = ctx.qp_active_set_batch(n, h, gd, go, c, x0, 6 * n + 10)
+    most = 0
+    for q in range(nqp):
+        ref = oracle.qp_active_set(n, h, gd[q].copy(), go[q].copy(), c[q].copy(), x0[q].copy(),
+                                   6 * n + 10)
+        assert out["status"][q] == ref["rc"], q
+        if ref["rc"] != 0:
+            continue
+        assert np.array_equal(out["x"][q], ref["x"]), q
+        assert np.array_equal(out["lam"][q], ref["lam"]), q
+        assert np.array_equal(out["sign"][q], ref["sign"]), q
+        assert out["iters"][q] == ref["iters"], q
+        most = max(most, int(np.count_nonzero(ref["sign"])))
+    assert most >= 10, most  # the Schur path really ran with sizable systems

@@ -159,3 +159,27 @@ def test_gn_c2_parity(ctx, oracle):
     for a, b in zip(o["rows"], r["rows"]):
         assert a["pcg_iters"] == b["pcg_iters"]
         assert a["j_value"] == pytest.approx(b["j_value"], rel=1e-9)
+
+
+@pytest.mark.parametrize("m", [(128, 9, 5), (256, 7, 3), (300, 5, 3), (512, 5, 2), (16, 7, 3)])
+@pytest.mark.parametrize("loop", ["1", "0"])
+def test_pcg_segmented_sweeps_bitwise(ctx, oracle, monkeypatch, m, loop):
+    """The block-Jacobi sweeps as warp-per-column segmented chains (pcg.cu
+    sweeps_seg: segments of 5 / 9 / 17 steps with agreement rounds, CPW 16
+    or 8) return the very bits of the thread-per-column chains
+    (EPC_PCG_SEG=0): d, the iteration count and relres identical, on column
+    lengths n1 = 129, 257, 301 and 513 and a short one, in the persistent
+    loop and in the per-iteration kernels."""
+    monkeypatch.setenv("EPC_PCG_LOOP", loop)
+    g, ip, im, _ = pair(m=m, scale=400.0)
+    rng = np.random.default_rng(8)
+    b = field(g, rng)
+    grad = oracle.objective_gn(g, ip, im, b)["grad"]
+    seg = ctx.pcg(g, ip, im, b, grad, 1e-4, 30, kind=abi.PRECOND_BLOCK_JACOBI)
+    monkeypatch.setenv("EPC_PCG_SEG", "0")
+    one = ctx.pcg(g, ip, im, b, grad, 1e-4, 30, kind=abi.PRECOND_BLOCK_JACOBI)
+    assert np.array_equal(seg["d"], one["d"])
+    assert seg["iters"] == one["iters"] and seg["relres"] == one["relres"]
+    r = oracle.pcg(g, ip, im, b, grad, 1e-4, 30, kind=abi.PRECOND_BLOCK_JACOBI)
+    assert seg["iters"] == r["iters"]
+    assert np.linalg.norm(seg["d"] - r["d"]) / np.linalg.norm(r["d"]) <= 1e-10
