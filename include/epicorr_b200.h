@@ -293,6 +293,22 @@ int epc_pcg(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
             const double* iminus, const double* b, const epc_objective_params* p, int kind,
             const double* grad, double eta, int max_iters, double* d, epc_pcg_result* out);
 
+/* The GN operators from a GnHessian's parts (the shim's GnHessian and
+ * make_preconditioner, objective.hpp:99-131, gn_pcg.hpp:47):
+ * GnHessian::apply (objective.cpp:302-331), y = T x + w2 (2x - x_{j+-1})
+ *   + w3 (2x - x_{k+-1}) with Neumann ends, from the column part diag/off;
+ * preconditioner_blocks().diag == full_diagonal() (objective.cpp:333-348),
+ *   out = diag + cross_diag(j, k);
+ * the Jacobi apply z = r / diag (gn_pcg.cpp:41-47) over n entries. The
+ * block-Jacobi apply is epc_tridiag_solve_batched on the preconditioner
+ * blocks. */
+int epc_gn_stencil_apply(epc_context* ctx, const epc_grid* g, int mem, const double* diag,
+                         const double* off, double w2, double w3, const double* x, double* y);
+int epc_gn_cross_diag_add(epc_context* ctx, const epc_grid* g, int mem, const double* diag,
+                          double w2, double w3, double* out);
+int epc_jacobi_apply(epc_context* ctx, long long n, int mem, const double* diag, const double* r,
+                     double* z);
+
 /* residual, objective.hpp:48, objective.cpp:77-91 (cells). */
 int epc_residual(epc_context* ctx, const epc_grid* g, int mem, const double* iplus,
                  const double* iminus, const double* b, double* r);
@@ -446,6 +462,45 @@ int epc_slab_zdiff(epc_context* ctx, const epc_grid* full, int k0, int mk, const
                    const double* halo, double* sums2);
 /* x *= factor (the u rescale after a rho change, admm.cpp:546-552). */
 int epc_slab_scale(epc_context* ctx, long long n, double* x, double factor);
+/* ---- multi-GPU variants of admm_solve ---------------------- */
+
+/* C4: npairs independent pairs (pair-major host arrays, as
+ * epc_admm_solve_batch) over a device list: contexts ctxs[0..nctx) (one per
+ * device), pairs split into contiguous balanced blocks, each block solved by
+ * epc_admm_solve_batch on its device from its own host thread. Results,
+ * rows and statuses land at the pairs' own offsets. No collective: pairs
+ * never couple. */
+int epc_admm_solve_batch_devices(epc_context* const* ctxs, int nctx, const epc_grid* g, int npairs,
+                                 const double* iplus, const double* iminus, const double* b_in,
+                                 const double* z_in, const double* u_in, double* b_out,
+                                 double* z_out, double* u_out, double* rho,
+                                 const epc_objective_params* p, const epc_admm_config* cfg,
+                                 int level_tag, epc_admm_row* rows, int max_rows,
+                                 epc_solve_status* status);
+
+/* NCCL communicator plumbing (NCCL is opened at run time): a 128-byte
+ * ncclUniqueId from rank 0, broadcast by the caller; one communicator per
+ * rank on `device`. comm is an ncclComm_t. */
+int epc_nccl_unique_id(char* out128);
+int epc_nccl_comm_create(int device, int world, int rank, const char* id128, void** comm);
+int epc_nccl_comm_destroy(void* comm);
+
+/* C5: admm_solve (admm.hpp:127-129) of ONE volume in k-slabs over the ranks
+ * of an NCCL communicator (comm may be NULL at world = 1). Rank r owns face
+ * layers [k0, k0 + mk) by shard_range over m3; ip/im are its cell slab,
+ * b_in/z_in/u_in (optional) and b_out/z_out/u_out its face slab, all DEVICE
+ * pointers on ctx's device. Per iteration: b-step, axis-2 DCT, a grouped
+ * ncclSend/ncclRecv all-to-all to i-slabs, axis-3 DCT + divide + inverse,
+ * the all-to-all back, inverse axis-2 DCT + dual update, a one-layer z halo
+ * from rank + 1, an ncclAllGather of 16 scalars; rows (replicated on every
+ * rank), stop test and rho schedule as epc_admm_solve. b, z, u are bitwise
+ * the single-GPU solve's (and the reference's) at every world size. */
+int epc_slab_admm_solve(epc_context* ctx, void* comm, int rank, int world, const epc_grid* full,
+                        const double* ip, const double* im, const double* b_in, const double* z_in,
+                        const double* u_in, double* b_out, double* z_out, double* u_out,
+                        double* rho, const epc_objective_params* p, const epc_admm_config* cfg,
+                        int level_tag, epc_admm_row* rows, int max_rows, epc_solve_status* status);
+
 /* The reference's five sequential dual-update sums (sum (b-z)^2, (zo-z)^2,
  * b^2, z^2, u^2 in index order, admm.cpp:461-469, grid.cpp:60-64) over n
  * faces, continuing the chains in io5[5] (host, in/out). The slab loop calls

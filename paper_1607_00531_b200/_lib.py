@@ -34,7 +34,9 @@ EXPORTS = [
     "epc_multilevel_solve", "epc_avg_x1", "epc_diff_x1", "epc_diff_x1_adjoint",
     "epc_smoother_hessian_apply", "epc_tridiag_apply", "epc_tridiag_solve_batched", "epc_dct_apply",
     "epc_distance_hessian_apply", "epc_is_strictly_feasible", "epc_correct_pair", "epc_ssd", "epc_ncc", "epc_simulate_pair", "epc_write_volume", "epc_read_volume",
-    "epc_permute_to_axis1", "epc_unpermute_field", "epc_admm_counters", "epc_slab_seq_sums", "epc_slab_d1_norm_inf",
+    "epc_permute_to_axis1", "epc_unpermute_field", "epc_admm_counters", "epc_slab_seq_sums", "epc_slab_d1_norm_inf", "epc_gn_stencil_apply", "epc_gn_cross_diag_add",
+    "epc_jacobi_apply", "epc_admm_solve_batch_devices", "epc_nccl_unique_id", "epc_nccl_comm_create",
+    "epc_nccl_comm_destroy", "epc_slab_admm_solve",
 ]
 
 
@@ -67,6 +69,17 @@ def _declare(L):
     L.epc_admm_counters.argtypes = [X, C.POINTER(C.c_longlong)]
     L.epc_slab_seq_sums.argtypes = [X, C.c_longlong, X, X, X, X, dptr]
     L.epc_slab_d1_norm_inf.argtypes = [X, G, C.c_int, C.c_int, X, dptr]
+    L.epc_gn_stencil_apply.argtypes = [X, G, C.c_int, X, X, C.c_double, C.c_double, X, X]
+    L.epc_gn_cross_diag_add.argtypes = [X, G, C.c_int, X, C.c_double, C.c_double, X]
+    L.epc_jacobi_apply.argtypes = [X, C.c_longlong, C.c_int, X, X, X]
+    L.epc_admm_solve_batch_devices.argtypes = [C.POINTER(C.c_void_p), C.c_int, G, C.c_int, X, X, X, X,
+                                               X, X, X, X, dptr, P, A, C.c_int, C.POINTER(AdmmRow),
+                                               C.c_int, C.POINTER(SolveStatus)]
+    L.epc_nccl_unique_id.argtypes = [C.c_char_p]
+    L.epc_nccl_comm_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]
+    L.epc_nccl_comm_destroy.argtypes = [X]
+    L.epc_slab_admm_solve.argtypes = [X, X, C.c_int, C.c_int, G, X, X, X, X, X, X, X, X, dptr, P, A,
+                                      C.c_int, C.POINTER(AdmmRow), C.c_int, C.POINTER(SolveStatus)]
     L.epc_profile_enable.argtypes = [X, C.c_int]
     L.epc_profile_read.argtypes = [X, C.POINTER(C.c_char_p), dptr, C.POINTER(C.c_long), C.c_int,
                                    C.POINTER(C.c_int)]

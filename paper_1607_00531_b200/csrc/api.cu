@@ -104,6 +104,7 @@ enum Slot {
     S_F32_IP, S_F32_IM, S_F32_B0, S_F32_B1, S_F32_Z0, S_F32_Z1, S_F32_U0, S_F32_U1, S_F32_T0,
     S_F32_T1, S_F32_MATS, S_F32_Q, S_F32_S, S_F32_COL, S_F32_SCAL, S_F32_PART,
     S_CTIME, S_SEQ,
+    S_SN0, S_SN1, S_SN2, S_SN3, S_SN4, S_SN5, S_SN6, S_SN7, S_SN8, S_SN9, S_SNH, S_SNG,
     S_COUNT
 };
 
@@ -1293,7 +1294,12 @@ int epc_qp_active_set_batch(epc_context* ctx, int nqp, int n, double h, const do
         double* dk = slot_t<double>(ctx, S_Z1, nqp);
         const size_t smem = bstep_smem_bytes(n);
         if (smem > ctx->smem_optin) fail(EPC_ERR_UNSUPPORTED, "QP too long for shared memory");
-        CK(cudaFuncSetAttribute(k_qp_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_optin));
+        // EPC_MODE_BSTEP_TIMING: the instrumented build, QP phase cycles into the
+        // b-step timing slot (epc_bstep_timing: factor, g, solves, Schur
+        // formation, Schur solve, p update, ratio test / append; dev aid)
+        const bool qdiag = (ctx->mode & EPC_MODE_BSTEP_TIMING) != 0;
+        void (*qk)(QpBatchParams) = qdiag ? k_qp_batch<true> : k_qp_batch<false>;
+        CK(cudaFuncSetAttribute(qk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_optin));
         const int blocks = std::min(nqp, ctx->num_sms * 8);
         const int qcap = n - 1;
         QpBatchParams P{};
@@ -1315,7 +1321,8 @@ int epc_qp_active_set_batch(epc_context* ctx, int nqp, int n, double h, const do
         P.sbuf = slot_t<double>(ctx, S_SBUF, (size_t)blocks * qcap * qcap);
         P.wbuf = slot_t<double>(ctx, S_X2, (size_t)blocks * 2 * n);
         P.qcap = qcap;
-        EPC_LAUNCH(ctx, "qp_batch", k_qp_batch, blocks, 32, smem, P);
+        P.timing = qdiag ? slot_t<long long>(ctx, S_GN9, 28) : nullptr;
+        EPC_LAUNCH(ctx, "qp_batch", qk, blocks, 32, smem, P);
         check_launch();
         std::vector<int> st(nqp);
         d2h(ctx, x, dx, nv * sizeof(double));
@@ -1364,4 +1371,5 @@ const char* epc_build_info(void) {
 #include "image_host.inc"
 #include "admm_f32_host.inc"
 #include "t2_host.inc"
+#include "multi_gpu_host.inc"
 

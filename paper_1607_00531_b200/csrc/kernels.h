@@ -50,7 +50,9 @@ struct QpBatchParams {
     int* status;
     double *qbuf, *sbuf, *wbuf;
     int qcap;
+    long long* timing;  // optional (the instrumented instantiation): QP phase cycles
 };
+template <bool DIAG>
 __global__ void k_qp_batch(QpBatchParams P);
 size_t bstep_smem_bytes(int n1, bool img_global = false);
 // Per-warp q-row scratch: qcap rows of n doubles plus CHAIN_PAD before and
@@ -203,7 +205,9 @@ __global__ void k_pcg_hvp(PcgHvArgs A, PcgState* S);
 void launch_pcg_update_bj(epc_context* ctx, int cpw, int seg, int blocks, size_t smem, const PcgUpdArgs& U,
                           PcgState* S);
 void set_pcg_update_bj_smem(int cpw, int seg, int bytes);
-bool pcg_variant_ok(int cpw, int seg);  // an instantiated (columns per block, segment) pair
+bool pcg_variant_ok(int cpw, int seg);
+int pcg_update_bj_per_sm(int cpw, int seg, size_t smem);  // after set_pcg_update_bj_smem
+int pcg_hvp_per_sm();  // an instantiated (columns per block, segment) pair
 struct PcgLoopArgs {
     PcgHvArgs H;
     PcgUpdArgs U;
@@ -310,6 +314,9 @@ void launch_diff_x1_adjoint(epc_context* ctx, const double* r, int m1, long long
                             double* out);
 void launch_smoother_apply(epc_context* ctx, const double* b, int m1, int m2, int m3,
                            long long nface, double w1, double w2, double w3, double* out);
+void launch_cross_diag_add(epc_context* ctx, const double* diag, int n1, int m2, int m3, int dim,
+                           long long nface, double w2, double w3, double* out);
+void launch_div_elem(epc_context* ctx, const double* r, const double* d, long long n, double* z);
 void launch_tridiag_apply(epc_context* ctx, const double* d, const double* o, const double* x,
                           int m1, long long nface, double s, double* y);
 void launch_tridiag_solve_cols(epc_context* ctx, const double* d, const double* o, double* fd,

@@ -252,3 +252,34 @@ int launch_d1_absmax(epc_context* ctx, const double* b, int m1, long long ncell,
     EPC_LAUNCH(ctx, "d1_absmax", k_d1_absmax, nb, 256, 0, b, m1, ncell, ih, part);
     return nb;
 }
+
+// GnHessian::preconditioner_blocks().diag == full_diagonal()
+// (objective.cpp:333-348): the column part's diagonal plus cross_diag(j, k)
+// (objective.cpp:296-300), w2 * (1 or 2) [+ w3 * (1 or 2) in 3D].
+__global__ void k_cross_diag_add(const double* diag, int n1, int m2, int m3, int dim,
+                                 long long nface, double w2, double w3, double* out) {
+    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < nface;
+         f += (long long)gridDim.x * blockDim.x) {
+        const long long c = f / n1;
+        const int j = (int)(c % m2), k = (int)(c / m2);
+        double cd = w2 * ((j == 0 || j == m2 - 1) ? 1.0 : 2.0);
+        if (dim == 3) cd += w3 * ((k == 0 || k == m3 - 1) ? 1.0 : 2.0);
+        out[f] = diag[f] + cd;
+    }
+}
+
+// the Jacobi preconditioner's apply (gn_pcg.cpp:41-47): z = r / diag
+__global__ void k_div_elem(const double* r, const double* d, long long n, double* z) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        z[i] = r[i] / d[i];
+}
+
+void launch_cross_diag_add(epc_context* ctx, const double* diag, int n1, int m2, int m3, int dim,
+                           long long nface, double w2, double w3, double* out) {
+    EPC_LAUNCH(ctx, "cross_diag_add", k_cross_diag_add, blocks_for(ctx, nface), 256, 0, diag, n1, m2,
+               m3, dim, nface, w2, w3, out);
+}
+void launch_div_elem(epc_context* ctx, const double* r, const double* d, long long n, double* z) {
+    EPC_LAUNCH(ctx, "div_elem", k_div_elem, blocks_for(ctx, n), 256, 0, r, d, n, z);
+}

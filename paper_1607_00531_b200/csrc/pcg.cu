@@ -293,7 +293,49 @@ __device__ __forceinline__ double ld_vec(const double* p) {
 }
 
 template <bool FIRST, bool COH>
-__device__ __forceinline__ void hvp_face(const PcgHvArgs& A, double beta, unsigned f, double& s) {
+__device__ __forceinline__ void hvp_face(const PcgHvArgs& A, double beta, unsigned f, double& xo,
+                                         double& yo) {
+    const double* __restrict__ Z = A.z;
+    const double* __restrict__ PO = A.p_old;
+    const unsigned n1 = A.n1, m1 = A.m1, m2 = A.m2, m3 = A.m3, layer = n1 * m2;
+    const unsigned c = f / n1, i = f - c * n1, k = c / m2, j = c - k * m2;
+    const bool bim = i > 0, bip = i < m1, bjm = j > 0, bjp = j + 1 < m2;
+    const bool bkm = m3 > 1 && k > 0, bkp = m3 > 1 && k + 1 < m3;
+    const unsigned fim = bim ? f - 1 : f, fip = bip ? f + 1 : f;
+    const unsigned fjm = bjm ? f - n1 : f, fjp = bjp ? f + n1 : f;
+    const unsigned fkm = bkm ? f - layer : f, fkp = bkp ? f + layer : f;
+    // all loads first (the seven z and p_old values, then diag / off), then
+    // p = z + beta p_old at the seven points
+    const unsigned idx[7] = {f, fim, fip, fjm, fjp, fkm, fkp};
+    double zv[7], pv[7];
+#pragma unroll
+    for (int t = 0; t < 7; ++t) zv[t] = ld_vec<COH>(Z + idx[t]);
+    if (!FIRST) {
+#pragma unroll
+        for (int t = 0; t < 7; ++t) pv[t] = ld_vec<COH>(PO + idx[t]);
+    }
+    const double dg = __ldg(A.diag + f), oim = __ldg(A.off + fim), oi = __ldg(A.off + f);
+    double xv[7];
+#pragma unroll
+    for (int t = 0; t < 7; ++t) xv[t] = FIRST ? zv[t] : zv[t] + beta * pv[t];
+    const double x = xv[0], xim = xv[1], xip = xv[2], xjm = xv[3], xjp = xv[4], xkm = xv[5],
+                 xkp = xv[6];
+    double acc = dg * x;
+    if (bim) acc += oim * xim;
+    if (bip) acc += oi * xip;
+    double y = acc;
+    if (bjm) y += A.w2 * (x - xjm);
+    if (bjp) y += A.w2 * (x - xjp);
+    if (bkm) y += A.w3 * (x - xkm);
+    if (bkp) y += A.w3 * (x - xkp);
+    xo = x;
+    yo = y;
+}
+
+// The loop kernel's form of one face (its 64-register cap): p at the seven
+// points formed as loaded, the stores right after (the PR-1 sequence).
+template <bool FIRST, bool COH>
+__device__ __forceinline__ void hvp_face_lean(const PcgHvArgs& A, double beta, unsigned f, double& s) {
     const double* __restrict__ Z = A.z;
     const double* __restrict__ PO = A.p_old;
     const unsigned n1 = A.n1, m1 = A.m1, m2 = A.m2, m3 = A.m3, layer = n1 * m2;
@@ -322,21 +364,62 @@ __device__ __forceinline__ void hvp_face(const PcgHvArgs& A, double beta, unsign
     s += x * y;
 }
 
+// EPC_HVP_UNROLL faces per thread in flight: every face's loads are issued
+// before any of their stores (the stores come last, so the compiler need
+// not assume they alias the next face's loads); s sums the faces in the
+// same order whatever the unroll.
+#ifndef EPC_HVP_UNROLL
+#define EPC_HVP_UNROLL 2
+#endif
+#ifndef EPC_HVP_LEAN_LOOP
+#define EPC_HVP_LEAN_LOOP 1
+#endif
 template <bool FIRST, bool COH>
 __device__ __forceinline__ double hvp_sweep(const PcgHvArgs& A, double beta) {
+    if (COH && EPC_HVP_LEAN_LOOP) {  // inside the persistent loop kernel
+        const unsigned n = A.n1 * A.m2 * A.m3;
+        const unsigned stride = gridDim.x * blockDim.x;
+        double s = 0.0;
+        unsigned f = blockIdx.x * blockDim.x + threadIdx.x;
+        for (; f + stride < n; f += 2 * stride) {
+            hvp_face_lean<FIRST, COH>(A, beta, f, s);
+            hvp_face_lean<FIRST, COH>(A, beta, f + stride, s);
+        }
+        if (f < n) hvp_face_lean<FIRST, COH>(A, beta, f, s);
+        return s;
+    }
+    constexpr int U = EPC_HVP_UNROLL;
     const unsigned n = A.n1 * A.m2 * A.m3;
     const unsigned stride = gridDim.x * blockDim.x;
+    double* __restrict__ PN = A.p_new;
+    double* __restrict__ Q = A.q;
     double s = 0.0;
     unsigned f = blockIdx.x * blockDim.x + threadIdx.x;
-    for (; f + stride < n; f += 2 * stride) {
-        hvp_face<FIRST, COH>(A, beta, f, s);
-        hvp_face<FIRST, COH>(A, beta, f + stride, s);
+    for (; f + (U - 1) * stride < n; f += U * stride) {
+        double x[U], y[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) hvp_face<FIRST, COH>(A, beta, f + u * stride, x[u], y[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            PN[f + u * stride] = x[u];
+            Q[f + u * stride] = y[u];
+            s += x[u] * y[u];
+        }
     }
-    if (f < n) hvp_face<FIRST, COH>(A, beta, f, s);
+    for (; f < n; f += stride) {
+        double x, y;
+        hvp_face<FIRST, COH>(A, beta, f, x, y);
+        PN[f] = x;
+        Q[f] = y;
+        s += x * y;
+    }
     return s;
 }
 
-__global__ void __launch_bounds__(256) k_pcg_hvp(PcgHvArgs A, PcgState* S) {
+#ifndef EPC_HVP_MINB
+#define EPC_HVP_MINB 1
+#endif
+__global__ void __launch_bounds__(256, EPC_HVP_MINB) k_pcg_hvp(PcgHvArgs A, PcgState* S) {
     __shared__ double sh[8];
     if (S->done) return;
     const double s = S->iters == 0 ? hvp_sweep<true, false>(A, 0.0) : hvp_sweep<false, false>(A, S->beta);
@@ -510,6 +593,17 @@ __device__ __forceinline__ void sweeps_seg(const PcgUpdArgs& A, int nc, double* 
     __syncthreads();
 }
 
+// This block's columns: an even-aligned, balanced share of the ncol columns
+// (pairs split evenly over the grid, so the 16-byte passes stay aligned and
+// no block does more than 2 ceil(ncol / 2 / grid) columns; equal-sized
+// rounds of CPW columns would leave blocks with a whole extra round).
+__device__ __forceinline__ void block_columns(long long ncol, long long& c0, long long& c1) {
+    const long long pairs = (ncol + 1) / 2, B = gridDim.x, b = blockIdx.x;
+    c0 = 2 * (pairs * b / B);
+    c1 = 2 * (pairs * (b + 1) / B);
+    if (c1 > ncol) c1 = ncol;
+}
+
 // 16-byte load; COH: written by other blocks of the same persistent kernel
 // (read through L2, not the incoherent L1 path).
 template <bool COH>
@@ -523,7 +617,7 @@ __device__ __forceinline__ double2 ld_vec2(const double* p) {
 // at face c0 n1 with c0 a multiple of CPW (even), and the span nc n1 is even
 // unless nc is odd (the last group), whose final face goes scalar.
 template <int CPW, bool UPD, bool COH, int SEG>
-__device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long long gi, double* X,
+__device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long long c0, int nc, double* X,
                                          double* Y, double& rr, double& rz) {
     const int tid = threadIdx.x;
     const int n1 = A.n1, RS = A.tile_rs;
@@ -536,8 +630,6 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
     const double* __restrict__ Qv = A.q;
     const double* __restrict__ FD = A.fd;
     const double* __restrict__ FL = A.fl;
-    const long long c0 = gi * CPW;
-    const int nc = (int)(A.ncol - c0 < CPW ? A.ncol - c0 : CPW);
     const size_t base = (size_t)c0 * n1;
     const int ne = nc * n1;
     const int ne2 = ne >> 1;
@@ -609,10 +701,11 @@ __global__ void __launch_bounds__(PCG_NT) k_pcg_update_bj(PcgUpdArgs A, PcgState
     double* const X = usm;
     double* const Y = X + CPW * A.tile_rs;
     const double a = S->alpha;
-    const long long ngroups = (A.ncol + CPW - 1) / CPW;
     double rr = 0.0, rz = 0.0;
-    for (long long gi = blockIdx.x; gi < ngroups; gi += gridDim.x)
-        bj_group<CPW, UPD, false, SEG>(A, a, gi, X, Y, rr, rz);
+    long long cb0, cb1;
+    block_columns(A.ncol, cb0, cb1);
+    for (long long c0 = cb0; c0 < cb1; c0 += CPW)
+        bj_group<CPW, UPD, false, SEG>(A, a, c0, (int)min((long long)CPW, cb1 - c0), X, Y, rr, rz);
     const double srr_b = block_sum(rr, sh);
     __syncthreads();
     const double srz_b = block_sum(rz, sh);
@@ -693,7 +786,8 @@ __global__ void __launch_bounds__(PCG_NT, EPC_PCG_LOOP_MINB) k_pcg_loop(PcgLoopA
     const int max_iters = S->max_iters;
     int reached = S->reached, err = 0;
     unsigned target = 0;
-    const long long ngroups = (L.U.ncol + CPW - 1) / CPW;
+    long long cb0, cb1;
+    block_columns(L.U.ncol, cb0, cb1);
     for (int k = 0; !done; ++k) {
         PcgHvArgs H = L.H;
         H.p_new = (k & 1) ? L.pbuf1 : L.pbuf0;
@@ -714,8 +808,9 @@ __global__ void __launch_bounds__(PCG_NT, EPC_PCG_LOOP_MINB) k_pcg_loop(PcgLoopA
         PcgUpdArgs U = L.U;
         U.p = H.p_new;
         double rr = 0.0, rzp = 0.0;
-        for (long long gi = blockIdx.x; gi < ngroups; gi += gridDim.x)
-            bj_group<CPW, true, true, SEG>(U, alpha, gi, X, Y, rr, rzp);
+        for (long long c0 = cb0; c0 < cb1; c0 += CPW)
+            bj_group<CPW, true, true, SEG>(U, alpha, c0, (int)min((long long)CPW, cb1 - c0), X, Y,
+                                           rr, rzp);
         const double srr_b = block_sum(rr, sh);
         __syncthreads();
         const double srz_b = block_sum(rzp, sh);
@@ -804,6 +899,22 @@ void launch_pcg_update_bj(epc_context* ctx, int cpw, int seg, int blocks, size_t
     }
     PCG_VARIANTS(PCG_LAUNCH_UPD)
 #undef PCG_LAUNCH_UPD
+}
+
+// resident blocks per SM of the per-iteration kernels (grids sized to one wave)
+int pcg_update_bj_per_sm(int cpw, int seg, size_t smem) {
+    int per = 0;
+#define PCG_OCC(C, SG)                                                                      \
+    if (cpw == C && seg == SG)                                                              \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_update_bj<C, true, SG>, PCG_NT, smem);
+    PCG_VARIANTS(PCG_OCC)
+#undef PCG_OCC
+    return per > 0 ? per : 1;
+}
+int pcg_hvp_per_sm() {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_hvp, 256, 0);
+    return per > 0 ? per : 1;
 }
 
 void set_pcg_update_bj_smem(int cpw, int seg, int bytes) {

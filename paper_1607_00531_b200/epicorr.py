@@ -214,6 +214,33 @@ class Context:
         return dict(b=bo, z=zo, u=uo, rho=r.value, stop=st.stop, message=st.message.decode(),
                     rows=abi.rows_to_dicts(rows, min(st.nrows, cfg.max_iter)))
 
+    def slab_admm_solve(self, comm, rank, world, g: Grid, ip, im, b=None, z=None, u=None, rho=0.0,
+                        params=None, cfg=None, level_tag=0):
+        """epc_slab_admm_solve: this rank's k-slab of one volume, NCCL between
+        the steps (comm: NcclComm or None at world 1). ip/im/b/z/u: this
+        rank's slabs as CUDA tensors. Returns the admm_solve dict (slabs)."""
+        import torch
+        params = params or ObjectiveParams()
+        cfg = cfg or AdmmConfig()
+        m1, m2, m3 = g.m
+        base, extra = divmod(m3, world)
+        mk = base + (1 if rank < extra else 0)
+        nf = (m1 + 1) * m2 * mk
+        bo, zo, uo = (torch.empty(nf, dtype=torch.float64, device=ip.device) for _ in range(3))
+        rows = (AdmmRow * max(cfg.max_iter, 1))()
+        st = SolveStatus()
+        r = C.c_double(rho)
+        torch.cuda.synchronize(ip.device)
+        P = self._ptr
+        rc = self.lib.epc_slab_admm_solve(self.h, comm.h if comm is not None else None, rank, world,
+                                          C.byref(g), P(ip), P(im), P(b), P(z), P(u), P(bo), P(zo),
+                                          P(uo), C.byref(r), C.byref(params), C.byref(cfg), level_tag,
+                                          rows, cfg.max_iter, C.byref(st))
+        if rc != 0:
+            _raise(rc, st.message.decode() or self._err())
+        return dict(b=bo, z=zo, u=uo, rho=r.value, stop=st.stop, message=st.message.decode(),
+                    rows=abi.rows_to_dicts(rows, min(st.nrows, cfg.max_iter)))
+
     def admm_solve_batch(self, g: Grid, npairs, ip, im, rho=None, params=None, cfg=None,
                          level_tag=0, b=None, z=None, u=None):
         """npairs independent admm_solve calls on one grid in the same kernels
@@ -375,6 +402,31 @@ class Context:
         self._check(self.lib.epc_tridiag_solve_batched(self.h, C.byref(g), mem, self._ptr(diag),
                                                        self._ptr(off), self._ptr(rhs), self._ptr(x)))
         return x
+
+    def gn_stencil_apply(self, g, diag, off, w2, w3, x):
+        """GnHessian::apply (objective.cpp:302-331) from the column part."""
+        mem = self._mem(diag, off, x)
+        y = self._like(x, g.faces)
+        self._check(self.lib.epc_gn_stencil_apply(self.h, C.byref(g), mem, self._ptr(diag),
+                                                  self._ptr(off), w2, w3, self._ptr(x), self._ptr(y)))
+        return y
+
+    def gn_cross_diag_add(self, g, diag, w2, w3):
+        """GnHessian::preconditioner_blocks().diag / full_diagonal() (objective.cpp:333-348)."""
+        mem = self._mem(diag)
+        out = self._like(diag, g.faces)
+        self._check(self.lib.epc_gn_cross_diag_add(self.h, C.byref(g), mem, self._ptr(diag), w2, w3,
+                                                   self._ptr(out)))
+        return out
+
+    def jacobi_apply(self, diag, r):
+        """The Jacobi preconditioner's apply, z = r / diag (gn_pcg.cpp:41-47)."""
+        mem = self._mem(diag, r)
+        n = len(r)
+        z = self._like(r, n)
+        self._check(self.lib.epc_jacobi_apply(self.h, n, mem, self._ptr(diag), self._ptr(r),
+                                              self._ptr(z)))
+        return z
 
     def dct_apply(self, g, z, alpha, rho):
         """DctCoupledSolver::apply (operators.cpp:420-446): Gt z."""
@@ -551,6 +603,64 @@ class Context:
 
 
 _default = None
+
+
+def admm_solve_batch_devices(contexts, g: Grid, npairs, ip, im, cfg=None, params=None, rho=None,
+                             b=None, z=None, u=None, level_tag=0):
+    """epc_admm_solve_batch_devices: npairs pairs (pair-major host arrays)
+    split over the contexts' devices, solved concurrently (no collective).
+    Returns dict(b, z, u, pairs) like Context.admm_solve_batch."""
+    lib = load()
+    params = params or ObjectiveParams()
+    cfg = cfg or AdmmConfig()
+    nf = g.faces * npairs
+    bo, zo, uo = np.zeros(nf), np.zeros(nf), np.zeros(nf)
+    rows = (AdmmRow * (max(cfg.max_iter, 1) * npairs))()
+    st = (SolveStatus * npairs)()
+    rh = (C.c_double * npairs)(*([0.0] * npairs if rho is None else rho))
+    hs = (C.c_void_p * len(contexts))(*[c.h.value for c in contexts])
+    P = lambda a: None if a is None else C.c_void_p(np.ascontiguousarray(a, np.float64).ctypes.data)
+    keep = [np.ascontiguousarray(a, np.float64) for a in (ip, im, b, z, u) if a is not None]
+    rc = lib.epc_admm_solve_batch_devices(hs, len(contexts), C.byref(g), npairs, P(ip), P(im), P(b),
+                                          P(z), P(u), C.c_void_p(bo.ctypes.data),
+                                          C.c_void_p(zo.ctypes.data), C.c_void_p(uo.ctypes.data), rh,
+                                          C.byref(params), C.byref(cfg), level_tag, rows,
+                                          cfg.max_iter, st)
+    del keep
+    if rc != 0:
+        _raise(rc, contexts[0]._err())
+    out = []
+    for q in range(npairs):
+        rr = [rows[q * cfg.max_iter + i] for i in range(min(st[q].nrows, cfg.max_iter))]
+        out.append(dict(stop=st[q].stop, message=st[q].message.decode(), rho=rh[q],
+                        rows=[{k: getattr(x, k) for k, _ in x._fields_} for x in rr]))
+    return dict(b=bo, z=zo, u=uo, pairs=out)
+
+
+def nccl_unique_id() -> bytes:
+    """epc_nccl_unique_id: 128 bytes to broadcast from rank 0."""
+    buf = C.create_string_buffer(128)
+    rc = load().epc_nccl_unique_id(buf)
+    if rc != 0:
+        _raise(rc, "epc_nccl_unique_id failed (NCCL unavailable?)")
+    return buf.raw
+
+
+class NcclComm:
+    """An NCCL communicator made by the library (epc_nccl_comm_create)."""
+
+    def __init__(self, device, world, rank, uid: bytes):
+        self.lib = load()
+        self.h = C.c_void_p()
+        rc = self.lib.epc_nccl_comm_create(device, world, rank, uid, C.byref(self.h))
+        if rc != 0:
+            _raise(rc, "epc_nccl_comm_create failed")
+        self.world, self.rank = world, rank
+
+    def close(self):
+        if self.h:
+            self.lib.epc_nccl_comm_destroy(self.h)
+            self.h = C.c_void_p()
 
 
 def context(device=0):

@@ -183,3 +183,34 @@ def test_pcg_segmented_sweeps_bitwise(ctx, oracle, monkeypatch, m, loop):
     r = oracle.pcg(g, ip, im, b, grad, 1e-4, 30, kind=abi.PRECOND_BLOCK_JACOBI)
     assert seg["iters"] == r["iters"]
     assert np.linalg.norm(seg["d"] - r["d"]) / np.linalg.norm(r["d"]) <= 1e-10
+
+
+@pytest.mark.parametrize("m,h", [((16, 12, 8), (1.0, 1.0, 1.0)), ((15, 9, 1), (0.8, 1.3, 1.0)),
+                                 ((12, 7, 5), (1.0, 0.7, 1.6))])
+def test_gn_operators_from_column_blocks(ctx, oracle, m, h):
+    """The C ABI behind the shim's GnHessian / make_preconditioner: the
+    stencil apply from the column part (GnHessian::apply), the
+    preconditioner-block diagonal (= full_diagonal()), the Jacobi apply and
+    the block-Jacobi apply (tridiag_solve_batched on the preconditioner
+    blocks), each bitwise against the oracle's own GnHessian pieces."""
+    d0 = synth.make_pair(synth.SynthSpec(m=m, seed=12))
+    g = abi.Grid.make(*m, h=h)
+    ip, im = d0.iplus * 400.0, d0.iminus * 400.0
+    rng = np.random.default_rng(3)
+    b = field(g, rng)
+    x = rng.uniform(-1, 1, g.faces)
+    params = abi.ObjectiveParams()
+    hb = oracle.gn_hessian_build(g, ip, im, b, params=params)
+    V = h[0] * h[1] * h[2]
+    w2 = params.alpha * V / (h[1] * h[1])
+    w3 = params.alpha * V / (h[2] * h[2]) if m[2] > 1 else 0.0
+    y = ctx.gn_stencil_apply(g, hb["diag"], hb["off"], w2, w3, x)
+    assert np.array_equal(y, oracle.gn_hessian_apply(g, ip, im, b, x, params=params))
+    pd = ctx.gn_cross_diag_add(g, hb["diag"], w2, w3)
+    assert np.array_equal(pd, hb["pdiag"])
+    r = rng.uniform(-1, 1, g.faces)
+    zj = ctx.jacobi_apply(pd, r)
+    assert np.array_equal(zj, oracle.precond_apply(g, ip, im, b, abi.PRECOND_JACOBI, r, params=params))
+    zb = ctx.tridiag_solve_batched(g, pd, hb["off"], r)
+    assert np.array_equal(zb, oracle.precond_apply(g, ip, im, b, abi.PRECOND_BLOCK_JACOBI, r,
+                                                   params=params))
