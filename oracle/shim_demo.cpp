@@ -15,6 +15,7 @@
 #include "epicorr/gn_pcg.hpp"
 #include "epicorr/image.hpp"
 #include "epicorr/multilevel.hpp"
+#include "epicorr/objective.hpp"
 
 using namespace epicorr;
 
@@ -64,6 +65,46 @@ int main(int argc, char** argv) {
                              double(mg.report.stop), double(ma.report.admm.size()),
                              double(mg.report.gn.size())};
     put(f, meta);
+    // the GN building blocks (objective_gn, GnHessian, make_preconditioner)
+    // driven through the reference's own generic pcg (gn_pcg.cpp:92-131)
+    const StaggeredField& bq = gsol.b;  // a feasible, nonzero field
+    const ObjectiveEval ev = objective_gn(pair, bq, p);
+    put(f, ev.grad.v);
+    put(f, ev.residual.v);
+    put(f, {ev.value, ev.dist, ev.smooth, ev.pen, double(ev.feasible)});
+    const GnHessian H(pair, bq, p);
+    put(f, H.apply(ev.grad).v);
+    put(f, H.preconditioner_blocks().diag);
+    put(f, H.full_diagonal());
+    const LinOp ah = [&](const std::vector<double>& x, std::vector<double>& y) {
+        y.resize(x.size());
+        H.apply(x, y);
+    };
+    for (PrecondKind kind : {PrecondKind::none, PrecondKind::jacobi, PrecondKind::block_jacobi,
+                             PrecondKind::sgs}) {
+        const LinOp m = make_preconditioner(kind, H);
+        std::vector<double> z;
+        m(ev.grad.v, z);
+        put(f, z);
+        const PcgResult pr = pcg(ah, m, ev.grad.v, 1e-3, 30);
+        put(f, pr.d);
+        put(f, {double(pr.iters), pr.relres, pr.relres_prec});
+    }
+    {  // dense() on a small grid (diagnostics)
+        const GridSpec gs = GridSpec::make3d(6, 5, 4);
+        SimulateOptions o2;
+        o2.seed = 3;
+        const VolumePair ps = simulate_pair(phantom_gaussian(gs), bump_field(gs, 0.3), o2);
+        const GnHessian Hs(ps, StaggeredField(gs), p);
+        put(f, Hs.dense());
+    }
+    // an infeasible point: +inf, no gradient
+    {
+        StaggeredField bad(g);
+        bad.v[1] = 5.0;
+        const ObjectiveEval e2 = objective_gn(pair, bad, p);
+        put(f, {e2.value, double(e2.feasible), double(e2.grad.v.size()), double(e2.residual.v.size())});
+    }
     std::fclose(f);
     std::printf("ok %zu admm rows, %zu ml-admm rows, %zu ml-gn rows\n", a.report.admm.size(),
                 ma.report.admm.size(), mg.report.gn.size());

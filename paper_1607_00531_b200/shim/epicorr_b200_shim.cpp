@@ -11,6 +11,13 @@
 //   augmented_lagrangian      (admm.hpp:87-89)
 //   qp_active_set             (admm.hpp:74-76)
 //   gauss_newton_solve        (proj/include/epicorr/gn_pcg.hpp:81-83)
+//   objective_gn              (proj/include/epicorr/objective.hpp:93-94)
+//   GnHessian                 (objective.hpp:99-131: ctor, apply, cross_diag,
+//                              preconditioner_blocks, full_diagonal, dense)
+//   make_preconditioner       (gn_pcg.hpp:47; none / jacobi / block_jacobi on
+//                              the device; sgs, sequential by design and out
+//                              of this build's scope, stays the reference's)
+//   multilevel_solve, restrict_image, prolong_field (multilevel.hpp)
 //
 // with the same signatures, ownership and exception behaviour (the C ABI's
 // status codes are rethrown as std::invalid_argument / std::runtime_error /
@@ -18,8 +25,10 @@
 // it in place of the reference's definitions of those functions; every other
 // reference translation unit (multilevel.cpp, the CLI, the tests) links
 // unchanged. INTEGRATION.md gives the recipe (the reference's admm.cpp /
-// gn_pcg.cpp stay in the build for their generic helpers, with the replaced
-// symbols renamed by -D at compile time).
+// gn_pcg.cpp / objective.cpp stay in the build for their generic helpers,
+// with the replaced symbols renamed by -D at compile time; objective.cpp's
+// GnHessian becomes ref_cpu_GnHessian there, and the shim defines the class's
+// members on the device).
 //
 // Device: EPICORR_B200_DEVICE (default 0); one context per process, created
 // on first use, owning its stream. Threading: the reference's free functions
@@ -36,6 +45,7 @@
 
 #include "epicorr/admm.hpp"
 #include "epicorr/gn_pcg.hpp"
+#include "epicorr/objective.hpp"
 #include "epicorr/multilevel.hpp"
 #include "epicorr_b200.h"
 
@@ -285,6 +295,153 @@ GnSolveResult gauss_newton_solve(const VolumePair& pair, const StaggeredField& b
     return out;
 }
 
+
+// ---- GN building blocks (objective.hpp:93-131, gn_pcg.hpp:47) ----------------
+
+ObjectiveEval objective_gn(const VolumePair& pair, const StaggeredField& b, const ObjectiveParams& p,
+                           int, bool need_grad) {
+    SHIM_LOCK;
+    p.validate();
+    const GridSpec& g = pair.grid();
+    if (!(b.grid == g)) throw std::invalid_argument("objective_gn: field grid mismatch");
+    const epc_grid cg = to_c(g);
+    const epc_objective_params cp = to_c(p);
+    std::vector<double> grad(g.faces()), res(g.cells());
+    epc_objective_eval ev{};
+    check(epc_objective_gn(ctx(), &cg, EPC_MEM_HOST, pair.plus.v.data(), pair.minus.v.data(),
+                           b.v.data(), &cp, need_grad ? 1 : 0, &ev, grad.data(), res.data()));
+    ObjectiveEval out;
+    out.value = ev.value;
+    out.dist = ev.dist;
+    out.smooth = ev.smooth;
+    out.pen = ev.pen;
+    out.feasible = ev.feasible != 0;
+    if (out.feasible) {  // objective.cpp:241-263: residual always, grad on request
+        out.residual = CellField(g);
+        out.residual.v = std::move(res);
+        if (need_grad) {
+            out.grad = StaggeredField(g);
+            out.grad.v = std::move(grad);
+        }
+    }
+    return out;
+}
+
+GnHessian::GnHessian(const VolumePair& pair, const StaggeredField& b, const ObjectiveParams& p,
+                     int threads)
+    : grid_(pair.grid()), col_(pair.grid()), threads_(threads) {
+    SHIM_LOCK;
+    p.validate();
+    const double V = grid_.cell_volume();
+    w2_ = p.alpha * V / (grid_.h[1] * grid_.h[1]);  // objective.cpp:271-272
+    w3_ = grid_.dim == 3 ? p.alpha * V / (grid_.h[2] * grid_.h[2]) : 0.0;
+    const epc_grid cg = to_c(grid_);
+    const epc_objective_params cp = to_c(p);
+    check(epc_gn_hessian_build(ctx(), &cg, EPC_MEM_HOST, pair.plus.v.data(), pair.minus.v.data(),
+                               b.v.data(), &cp, col_.diag.data(), col_.off.data(), nullptr));
+}
+
+double GnHessian::cross_diag(int j, int k) const {  // objective.cpp:296-300 (a scalar)
+    double d = w2_ * ((j == 0 || j == grid_.m[1] - 1) ? 1.0 : 2.0);
+    if (grid_.dim == 3) d += w3_ * ((k == 0 || k == grid_.m[2] - 1) ? 1.0 : 2.0);
+    return d;
+}
+
+void GnHessian::apply(std::span<const double> x, std::span<double> y) const {
+    SHIM_LOCK;
+    const epc_grid cg = to_c(grid_);
+    check(epc_gn_stencil_apply(ctx(), &cg, EPC_MEM_HOST, col_.diag.data(), col_.off.data(), w2_, w3_,
+                               x.data(), y.data()));
+}
+
+StaggeredField GnHessian::apply(const StaggeredField& x) const {
+    StaggeredField out(grid_);
+    apply(x.v, out.v);
+    return out;
+}
+
+TridiagBlocks GnHessian::preconditioner_blocks() const {
+    SHIM_LOCK;
+    TridiagBlocks t = col_;
+    const epc_grid cg = to_c(grid_);
+    check(epc_gn_cross_diag_add(ctx(), &cg, EPC_MEM_HOST, col_.diag.data(), w2_, w3_, t.diag.data()));
+    return t;
+}
+
+std::vector<double> GnHessian::full_diagonal() const {
+    SHIM_LOCK;
+    std::vector<double> d(col_.diag.size());
+    const epc_grid cg = to_c(grid_);
+    check(epc_gn_cross_diag_add(ctx(), &cg, EPC_MEM_HOST, col_.diag.data(), w2_, w3_, d.data()));
+    return d;
+}
+
+// Dense row-major assembly for small-problem diagnostics (objective.cpp:
+// 350-384): the values are the device's (full_diagonal, the column part's
+// off-diagonals, the cross weights); the host only places them.
+std::vector<double> GnHessian::dense() const {
+    const std::int64_t n = grid_.faces();
+    const int n1 = grid_.n1(), m2 = grid_.m[1], m3 = grid_.m[2];
+    const std::vector<double> dg = full_diagonal();
+    std::vector<double> a(std::size_t(n) * n, 0.0);
+    const std::int64_t layer = std::int64_t(n1) * m2;
+    for (std::int64_t f = 0; f < n; ++f) {
+        const std::int64_t c = f / n1;
+        const int i = int(f % n1), j = int(c % m2), k = int(c / m2);
+        a[std::size_t(f) * n + f] = dg[f];
+        if (i + 1 < n1) {
+            a[std::size_t(f) * n + f + 1] = col_.off[f];
+            a[std::size_t(f + 1) * n + f] = col_.off[f];
+        }
+        if (j > 0) a[std::size_t(f) * n + (f - n1)] = -w2_;
+        if (j + 1 < m2) a[std::size_t(f) * n + (f + n1)] = -w2_;
+        if (m3 > 1) {
+            if (k > 0) a[std::size_t(f) * n + (f - layer)] = -w3_;
+            if (k + 1 < m3) a[std::size_t(f) * n + (f + layer)] = -w3_;
+        }
+    }
+    return a;
+}
+
+// the reference's own make_preconditioner (gn_pcg.cpp, compiled renamed):
+// the symmetric Gauss-Seidel sweeps are sequential by design
+LinOp ref_cpu_make_preconditioner(PrecondKind kind, const GnHessian& h, int threads);
+
+LinOp make_preconditioner(PrecondKind kind, const GnHessian& h, int threads) {
+    switch (kind) {
+        case PrecondKind::none:
+            return [](const std::vector<double>& r, std::vector<double>& z) { z = r; };
+        case PrecondKind::jacobi: {  // gn_pcg.cpp:41-47
+            auto diag = h.full_diagonal();
+            return [diag](const std::vector<double>& r, std::vector<double>& z) {
+                SHIM_LOCK;
+                z.resize(r.size());
+                check(epc_jacobi_apply(ctx(), (long long)r.size(), EPC_MEM_HOST, diag.data(), r.data(),
+                                       z.data()));
+            };
+        }
+        case PrecondKind::block_jacobi: {  // gn_pcg.cpp:48-54
+            const TridiagBlocks t = h.preconditioner_blocks();
+            const epc_grid cg = to_c(h.grid());
+            {
+                // TridiagFactor::factorize throws here (operators.cpp:230-240), not at apply
+                SHIM_LOCK;
+                std::vector<double> zero(t.diag.size(), 0.0), x(t.diag.size());
+                check(epc_tridiag_solve_batched(ctx(), &cg, EPC_MEM_HOST, t.diag.data(), t.off.data(),
+                                                zero.data(), x.data()));
+            }
+            return [t, cg](const std::vector<double>& r, std::vector<double>& z) {
+                SHIM_LOCK;
+                z.resize(r.size());
+                check(epc_tridiag_solve_batched(ctx(), &cg, EPC_MEM_HOST, t.diag.data(), t.off.data(),
+                                                r.data(), z.data()));
+            };
+        }
+        case PrecondKind::sgs:
+            return ref_cpu_make_preconditioner(kind, h, threads);
+    }
+    throw std::logic_error("make_preconditioner: bad kind");
+}
 
 // ---- multilevel (multilevel.hpp:37-63) on the device --------------------------
 ImageVolume restrict_image(const ImageVolume& img, const GridSpec& coarse) {

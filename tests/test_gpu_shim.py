@@ -32,7 +32,7 @@ def test_shim_drop_in_matches_reference(tmp_path):
     subprocess.run([REF, a], check=True, timeout=600)
     subprocess.run([SHIM, b], check=True, timeout=600)
     r, g = read(a), read(b)
-    assert len(r) == len(g) == 8
+    assert len(r) == len(g) == 8 + 6 + 4 * 3 + 2
     # single-level ADMM: b, z, u bitwise; Lagrangian rows within tree-sum rounding
     for k in range(3):
         assert np.array_equal(g[k], r[k]), k
@@ -44,3 +44,17 @@ def test_shim_drop_in_matches_reference(tmp_path):
     # ... and over the GPU GN
     assert np.linalg.norm(g[6] - r[6]) <= 1e-8 * np.linalg.norm(r[6])
     assert np.array_equal(g[7], r[7])  # stop reasons and row counts
+    # objective_gn, GnHessian (apply, preconditioner_blocks, full_diagonal),
+    # make_preconditioner (none / jacobi / block_jacobi on the device, sgs the
+    # reference's) and the reference's own pcg over them: bitwise; the
+    # objective's scalar sums within their tree-sum rounding
+    for k in (8, 9, 11, 12, 13):
+        assert np.array_equal(g[k], r[k]), k
+    assert np.allclose(g[10], r[10], rtol=1e-12, atol=0)
+    for q in range(4):
+        z, d, meta = 14 + 3 * q, 15 + 3 * q, 16 + 3 * q
+        assert np.array_equal(g[z], r[z]), ("precond", q)
+        assert np.array_equal(g[d], r[d]), ("pcg", q)
+        assert np.array_equal(g[meta], r[meta]), ("pcg meta", q)
+    assert np.array_equal(g[26], r[26])  # GnHessian::dense
+    assert np.array_equal(g[27], r[27])  # infeasible: +inf, feasible 0, empty grad/residual
