@@ -70,7 +70,9 @@ def parse():
 # fp64 DADD/DMUL issue rate measured on this pool (profiles/r01_ubench_fp64_tput.log)
 FP64_PEAK_TOPS = 18.3
 NCU_BSTEP_SUMMARY = "r01o_bstep_ncu.json"  # C3 b-step, one launch, ncu --set full
-NCU_PCG_SUMMARY = {"C2": "r02_pcg_c2_ncu.json", "C3": "r02_pcg_c3_ncu.json"}  # k_pcg_loop captures
+# the GN-PCG kernels' ncu captures: C2 runs the persistent loop (L2-resident),
+# C3 the per-iteration kernels (k_pcg_hvp, k_pcg_update_bj)
+NCU_PCG_SUMMARY = {"C2": "r02_pcg_c2_ncu.json", "C3": "r02_pcg_parts_c3_ncu.json"}
 DEFAULT_ITERS = {"C1": 50, "C2": 50, "C3": 100, "C4": 50, "C5": 50}
 
 
@@ -422,17 +424,24 @@ def run_gn_leg(a, ctx, dev, stream, flush, rank, dist, config_name, cpu_windows,
             src = "measured"
         except Exception:
             peak, src = 6650.0, "fallback"
-        traffic, tsrc = None, None
+        traffic, tsrc, tunit = None, None, None
         cap_name = NCU_PCG_SUMMARY.get(config_name)
-        try:  # DRAM bytes per PCG iteration of the loop kernel from the committed capture
+        try:  # DRAM bytes from the committed ncu --set full capture of the same kernel
             cap = json.load(open(os.path.join(ROOT, "profiles", cap_name)))
-            traffic = float(cap["dram_bytes_per_pcg_iteration"])
+            if top["kernel"] == "pcg_loop":
+                traffic, tunit = float(cap["dram_bytes_per_pcg_iteration"]), "bytes per PCG iteration"
+            else:
+                traffic = float(cap["kernels"][top["kernel"]]["dram_bytes_per_launch"])
+                tunit = "bytes per launch"
             tsrc = "profiles/" + cap_name
         except Exception:
             pass
+        for k in kernels:  # every PCG kernel's own fraction of the roof
+            if "achieved_gbs" in k:
+                k["frac_hbm"] = k["achieved_gbs"] / peak
         roof = {"bound": "hbm", "kernel": top["kernel"], "achieved": top["achieved_gbs"], "peak": peak,
                 "peak_source": src, "unit": "GB/s", "frac": top["achieved_gbs"] / peak,
-                "traffic": traffic, "traffic_unit": "bytes per PCG iteration",
+                "traffic": traffic, "traffic_unit": tunit, "alg_bytes": top["alg_bytes"],
                 "alg_bytes_per_pcg_iteration": 120 * g.faces, "traffic_source": tsrc,
                 "note": ("algorithmic bytes (120 B/face per PCG iteration) / CUDA-event time; " +
                          ("the PCG vectors fit in L2 at this size" if fits_l2 else

@@ -168,6 +168,10 @@ int epc_set_mode(epc_context* ctx, int mode_bits);
  * sequential sums (undecidable enclosure, or EPC_MODE_EXACT_SUMS),
  * out4[2] b-step SQP iterations, out4[3] QP iterations (BUpdateStats sums). */
 int epc_admm_counters(epc_context* ctx, long long* out4);
+/* Guard mode (dev aid; EPC_GUARD=1 in the environment when the context is
+ * created): every device scratch slot carries 4 KB guard zones; this checks
+ * them all and returns the first overwritten slot in *bad_slot (-1: none). */
+int epc_guard_check(epc_context* ctx, int* bad_slot);
 /* Phase cycle totals of the b-step kernel since timing was enabled (lane 0
  * clock64 deltas): model, fval sums, factor, solves, QP rest, KKT, step
  * sums, line search, clamp+store, column fetch. */

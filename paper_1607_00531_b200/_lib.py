@@ -36,7 +36,7 @@ EXPORTS = [
     "epc_distance_hessian_apply", "epc_is_strictly_feasible", "epc_correct_pair", "epc_ssd", "epc_ncc", "epc_simulate_pair", "epc_write_volume", "epc_read_volume",
     "epc_permute_to_axis1", "epc_unpermute_field", "epc_admm_counters", "epc_slab_seq_sums", "epc_slab_d1_norm_inf", "epc_gn_stencil_apply", "epc_gn_cross_diag_add",
     "epc_jacobi_apply", "epc_admm_solve_batch_devices", "epc_nccl_unique_id", "epc_nccl_comm_create",
-    "epc_nccl_comm_destroy", "epc_slab_admm_solve",
+    "epc_nccl_comm_destroy", "epc_slab_admm_solve", "epc_guard_check",
 ]
 
 
@@ -76,6 +76,7 @@ def _declare(L):
                                                X, X, X, X, dptr, P, A, C.c_int, C.POINTER(AdmmRow),
                                                C.c_int, C.POINTER(SolveStatus)]
     L.epc_nccl_unique_id.argtypes = [C.c_char_p]
+    L.epc_guard_check.argtypes = [X, C.POINTER(C.c_int)]
     L.epc_nccl_comm_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]
     L.epc_nccl_comm_destroy.argtypes = [X]
     L.epc_slab_admm_solve.argtypes = [X, X, C.c_int, C.c_int, G, X, X, X, X, X, X, X, X, dptr, P, A,

@@ -108,18 +108,31 @@ enum Slot {
     S_COUNT
 };
 
+// Guard mode (EPC_GUARD=1 when the context is created; dev aid standing in
+// for compute-sanitizer, which this pool does not run): every scratch slot
+// gets a 4 KB zone of 0xA5 bytes on each side, checked by epc_guard_check
+// after the work (an out-of-bounds write to any scratch buffer shows there).
+constexpr size_t GUARD_BYTES = 4096;
+
 void* slot(epc_context* ctx, int s, size_t bytes) {
     if ((int)ctx->bufs.size() < S_COUNT) ctx->bufs.resize(S_COUNT);
     DevBuf& b = ctx->bufs[s];
+    const size_t g = ctx->guard ? GUARD_BYTES : 0;
     if (b.bytes < bytes) {
         if (b.ptr) {
             CK(cudaStreamSynchronize(ctx->stream));
-            CK(cudaFree(b.ptr));
+            CK(cudaFree(static_cast<char*>(b.ptr) - g));
             b.ptr = nullptr;
             b.bytes = 0;
         }
-        const size_t want = std::max<size_t>(bytes, 256);
-        CK(cudaMalloc(&b.ptr, want));
+        const size_t want = (std::max<size_t>(bytes, 256) + 255) / 256 * 256;
+        char* raw = nullptr;
+        CK(cudaMalloc(&raw, want + 2 * g));
+        if (g) {
+            CK(cudaMemsetAsync(raw, 0xA5, g, ctx->stream));
+            CK(cudaMemsetAsync(raw + g + want, 0xA5, g, ctx->stream));
+        }
+        b.ptr = raw + g;
         b.bytes = want;
     }
     return b.ptr;
@@ -548,6 +561,7 @@ const char* qp_what(int code) {
         case 2: return "qp_active_set: infeasible starting point";
         case 3: return "qp_active_set: singular Schur complement";
         case 4: return "qp_active_set: iteration cap reached (cycling guard)";
+        case 9: return "shared-memory canary overwritten (EPC_SMEM_CANARY build)";
     }
     return "unknown column failure";
 }
@@ -976,6 +990,7 @@ int epc_context_create(int device, void* stream, epc_context** out) {
         CK(cudaGetDeviceProperties(&prop, device));
         if (prop.major != 10) fail(EPC_ERR_UNSUPPORTED, std::string("libepicorr_b200 is built for sm_100a; device is ") + prop.name);
         ctx->num_sms = prop.multiProcessorCount;
+        ctx->guard = getenv("EPC_GUARD") && atoi(getenv("EPC_GUARD")) != 0;
         ctx->smem_optin = prop.sharedMemPerBlockOptin;
         if (stream) {
             ctx->stream = static_cast<cudaStream_t>(stream);
@@ -999,7 +1014,7 @@ void epc_context_destroy(epc_context* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (auto& b : ctx->bufs)
-        if (b.ptr) cudaFree(b.ptr);
+        if (b.ptr) cudaFree(static_cast<char*>(b.ptr) - (ctx->guard ? GUARD_BYTES : 0));
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->pinned_aux) cudaFreeHost(ctx->pinned_aux);
     for (auto& pe : ctx->prof_pending) {
@@ -1079,6 +1094,31 @@ void epc_profile_reset(epc_context* ctx) {
 }
 
 long epc_launch_count(const epc_context* ctx) { return ctx->launches; }
+
+int epc_guard_check(epc_context* ctx, int* bad_slot) {
+    return guarded(ctx, [&] {
+        *bad_slot = -1;
+        if (!ctx->guard) fail(EPC_ERR_UNSUPPORTED, "guard_check: context not created with EPC_GUARD=1");
+        int* flag = static_cast<int*>(pinned_aux(ctx));
+        for (int sidx = 0; sidx < (int)ctx->bufs.size() && *bad_slot < 0; ++sidx) {
+            const DevBuf& b = ctx->bufs[sidx];
+            if (!b.ptr) continue;
+            const unsigned char* lo = static_cast<const unsigned char*>(b.ptr) - GUARD_BYTES;
+            const unsigned char* hi = static_cast<const unsigned char*>(b.ptr) + b.bytes;
+            for (const unsigned char* z : {lo, hi}) {
+                std::vector<unsigned char> h(GUARD_BYTES);
+                CK(cudaMemcpyAsync(h.data(), z, GUARD_BYTES, cudaMemcpyDeviceToHost, ctx->stream));
+                sync(ctx);
+                for (unsigned char c : h)
+                    if (c != 0xA5) {
+                        *bad_slot = sidx;
+                        break;
+                    }
+            }
+        }
+        (void)flag;
+    });
+}
 
 int epc_admm_counters(epc_context* ctx, long long* out4) {
     if (!ctx || !out4) return EPC_ERR_INVALID_ARGUMENT;

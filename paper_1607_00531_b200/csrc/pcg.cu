@@ -643,11 +643,14 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
         X[k] = r0;
         Y[k] = l0;
     };
+    // Per-iteration kernel: two face pairs per thread, all ten 16-byte loads
+    // issued before any store (the compiler does not move loads across the d
+    // / r stores itself). The loop kernel (64-register cap) keeps the lean form.
+    if constexpr (COH) {
 #pragma unroll 2
-    for (int h = tid; h < ne2; h += PCG_NT) {
-        const size_t o = base + 2 * (size_t)h;
-        double2 r = *reinterpret_cast<const double2*>(Rv + o);
-        if (UPD) {
+        for (int h = tid; h < ne2; h += PCG_NT) {
+            const size_t o = base + 2 * (size_t)h;
+            double2 r = *reinterpret_cast<const double2*>(Rv + o);
             const double2 pp = ld_vec2<COH>(Pv + o), qq = ld_vec2<COH>(Qv + o);
             double2 dd = *reinterpret_cast<const double2*>(Dv + o);
             dd.x = dd.x + a * pp.x;
@@ -656,10 +659,40 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
             r.y += ma * qq.y;
             *reinterpret_cast<double2*>(Dv + o) = dd;
             *reinterpret_cast<double2*>(Rv + o) = r;
+            const double2 l = __ldg(reinterpret_cast<const double2*>(FL + o));
+            stage1(2 * h, r.x, l.x);
+            stage1(2 * h + 1, r.y, l.y);
         }
-        const double2 l = __ldg(reinterpret_cast<const double2*>(FL + o));
-        stage1(2 * h, r.x, l.x);
-        stage1(2 * h + 1, r.y, l.y);
+    } else for (int h0 = tid; h0 < ne2; h0 += 2 * PCG_NT) {
+        double2 r[2], pp[2], qq[2], dd[2], l[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int h = min(h0 + u * PCG_NT, ne2 - 1);
+            const size_t o = base + 2 * (size_t)h;
+            r[u] = *reinterpret_cast<const double2*>(Rv + o);
+            if (UPD) {
+                pp[u] = ld_vec2<COH>(Pv + o);
+                qq[u] = ld_vec2<COH>(Qv + o);
+                dd[u] = *reinterpret_cast<const double2*>(Dv + o);
+            }
+            l[u] = __ldg(reinterpret_cast<const double2*>(FL + o));
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int h = h0 + u * PCG_NT;
+            if (h >= ne2) break;
+            const size_t o = base + 2 * (size_t)h;
+            if (UPD) {
+                dd[u].x = dd[u].x + a * pp[u].x;
+                dd[u].y = dd[u].y + a * pp[u].y;
+                r[u].x += ma * qq[u].x;
+                r[u].y += ma * qq[u].y;
+                *reinterpret_cast<double2*>(Dv + o) = dd[u];
+                *reinterpret_cast<double2*>(Rv + o) = r[u];
+            }
+            stage1(2 * h, r[u].x, l[u].x);
+            stage1(2 * h + 1, r[u].y, l[u].y);
+        }
     }
     if ((ne & 1) && tid == 0) {
         const size_t o = base + ne - 1;
@@ -675,14 +708,30 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
     __syncthreads();
     if (SEG) sweeps_seg<SEG, CPW>(A, nc, X, Y, base, sidx, ne, ne2);
     else sweeps_thread(A, nc, X, Y, base, sidx, ne, ne2);
+    if constexpr (COH) {
 #pragma unroll 2
-    for (int h = tid; h < ne2; h += PCG_NT) {
-        const size_t o = base + 2 * (size_t)h;
-        const double2 r = *reinterpret_cast<const double2*>(Rv + o);
-        const double2 z = make_double2(X[sidx(2 * h)], X[sidx(2 * h + 1)]);
-        *reinterpret_cast<double2*>(Zv + o) = z;
-        rz += r.x * z.x;
-        rz += r.y * z.y;
+        for (int h = tid; h < ne2; h += PCG_NT) {
+            const size_t o = base + 2 * (size_t)h;
+            const double2 r = *reinterpret_cast<const double2*>(Rv + o);
+            const double2 z = make_double2(X[sidx(2 * h)], X[sidx(2 * h + 1)]);
+            *reinterpret_cast<double2*>(Zv + o) = z;
+            rz += r.x * z.x;
+            rz += r.y * z.y;
+        }
+    } else for (int h0 = tid; h0 < ne2; h0 += 2 * PCG_NT) {  // loads of both pairs first
+        double2 r[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            r[u] = *reinterpret_cast<const double2*>(Rv + base + 2 * (size_t)min(h0 + u * PCG_NT, ne2 - 1));
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int h = h0 + u * PCG_NT;
+            if (h >= ne2) break;
+            const double2 z = make_double2(X[sidx(2 * h)], X[sidx(2 * h + 1)]);
+            *reinterpret_cast<double2*>(Zv + base + 2 * (size_t)h) = z;
+            rz += r[u].x * z.x;
+            rz += r[u].y * z.y;
+        }
     }
     if ((ne & 1) && tid == 0) {
         const size_t o = base + ne - 1;
@@ -808,9 +857,15 @@ __global__ void __launch_bounds__(PCG_NT, EPC_PCG_LOOP_MINB) k_pcg_loop(PcgLoopA
         PcgUpdArgs U = L.U;
         U.p = H.p_new;
         double rr = 0.0, rzp = 0.0;
-        for (long long c0 = cb0; c0 < cb1; c0 += CPW)
-            bj_group<CPW, true, true, SEG>(U, alpha, c0, (int)min((long long)CPW, cb1 - c0), X, Y,
-                                           rr, rzp);
+        if (U.bal) {
+            for (long long c0 = cb0; c0 < cb1; c0 += CPW)
+                bj_group<CPW, true, true, SEG>(U, alpha, c0, (int)min((long long)CPW, cb1 - c0), X, Y,
+                                               rr, rzp);
+        } else {  // whole groups of CPW columns, round-robin over the blocks
+            for (long long c0 = (long long)blockIdx.x * CPW; c0 < U.ncol; c0 += (long long)gridDim.x * CPW)
+                bj_group<CPW, true, true, SEG>(U, alpha, c0, (int)min((long long)CPW, U.ncol - c0), X, Y,
+                                               rr, rzp);
+        }
         const double srr_b = block_sum(rr, sh);
         __syncthreads();
         const double srz_b = block_sum(rzp, sh);
@@ -850,9 +905,9 @@ __global__ void __launch_bounds__(PCG_NT, EPC_PCG_LOOP_MINB) k_pcg_loop(PcgLoopA
 }
 
 // Cooperative launch of the loop; false when the device cannot hold the grid.
-// (CPW, SEG) instantiations: 16 columns per block only for n1 <= ~160
-// (segment 5 covers them), 8 for longer columns (segments 9, 17)
-#define PCG_VARIANTS(X) X(16, 0) X(16, 5) X(8, 0) X(8, 9) X(8, 17)
+// (CPW, SEG) instantiations: 16 columns per block (n1 <= ~160) keep the
+// thread chains; 8 for longer columns, segments 9 or 17
+#define PCG_VARIANTS(X) X(16, 0) X(8, 0) X(8, 9) X(8, 17)
 
 static const void* pcg_loop_fn(int cpw, int seg) {
 #define PCG_PICK(C, S) if (cpw == C && seg == S) return (const void*)k_pcg_loop<C, S>;

@@ -136,6 +136,13 @@ class Context:
     MODE_BSTEP_CHAINED = 1 << 13
     MODE_EXACT_SUMS = 1 << 14
 
+    def guard_check(self):
+        """First scratch slot whose guard zones were overwritten, or -1
+        (contexts created with EPC_GUARD=1)."""
+        b = C.c_int(-1)
+        self._check(self.lib.epc_guard_check(self.h, C.byref(b)))
+        return b.value
+
     def admm_counters(self):
         """Cumulative (decisions certified from the tree sums, decisions taken
         on the reference's exact sequential sums, SQP iterations, QP iterations)."""

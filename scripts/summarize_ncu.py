@@ -88,7 +88,32 @@ def pcg(src, dst, pcg_iters, faces):
     json.dump(d, open(dst, "w"), indent=1)
 
 
+def parts(src, dst, faces):
+    """captures of the per-iteration PCG kernels (k_pcg_hvp, k_pcg_update_bj):
+    DRAM bytes and time per launch against their algorithmic bytes (48 and
+    72 B/face)."""
+    capture(src, dst)
+    d = json.load(open(dst))
+    d = d if isinstance(d, list) else [d]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tu = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "us": 1e-6, "ms": 1e-3}
+    out = {"faces": int(faces), "kernels": {}, "captures": d}
+    for x in d:
+        name = "pcg_hvp" if "pcg_hvp" in x["Kernel Name"][0] else "pcg_update"
+        b = sum(float(x[k][0].replace(",", "")) * scale[x[k][1]]
+                for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        t = float(x["gpu__time_duration.sum"][0].replace(",", "")) * tu[x["gpu__time_duration.sum"][1]]
+        alg = (48 if name == "pcg_hvp" else 72) * int(faces)
+        out["kernels"][name] = {"dram_bytes_per_launch": b, "alg_bytes_per_launch": alg,
+                                "traffic_over_alg": b / alg, "seconds_under_ncu": t,
+                                "dram_gbs_under_ncu": b / t / 1e9}
+    json.dump(out, open(dst, "w"), indent=1)
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "parts":
+        parts(*sys.argv[2:5])
+        sys.exit(0)
     if sys.argv[1] == "pcg":
         pcg(*sys.argv[2:6])
     else:
