@@ -196,7 +196,6 @@ struct PcgUpdArgs {
     long long ncol;
     double* partials;
     int tile_rs;  // k_pcg_update_bj: shared-memory row stride (odd, >= n1)
-    int bal;      // loop kernel: balanced column ranges per block (1) or whole groups round-robin (0)
     int seg;      // block-Jacobi sweeps: segment length of the warp-per-column chains
                   // (5, 9 or 17; three staged arrays), 0 = thread-per-column chains
 };

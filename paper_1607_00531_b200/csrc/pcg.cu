@@ -376,7 +376,7 @@ __device__ __forceinline__ void hvp_face_lean(const PcgHvArgs& A, double beta, u
 #endif
 template <bool FIRST, bool COH>
 __device__ __forceinline__ double hvp_sweep(const PcgHvArgs& A, double beta) {
-    if (COH && EPC_HVP_LEAN_LOOP) {  // inside the persistent loop kernel
+    if constexpr (COH && EPC_HVP_LEAN_LOOP) {  // inside the persistent loop kernel
         const unsigned n = A.n1 * A.m2 * A.m3;
         const unsigned stride = gridDim.x * blockDim.x;
         double s = 0.0;
@@ -835,8 +835,6 @@ __global__ void __launch_bounds__(PCG_NT, EPC_PCG_LOOP_MINB) k_pcg_loop(PcgLoopA
     const int max_iters = S->max_iters;
     int reached = S->reached, err = 0;
     unsigned target = 0;
-    long long cb0, cb1;
-    block_columns(L.U.ncol, cb0, cb1);
     for (int k = 0; !done; ++k) {
         PcgHvArgs H = L.H;
         H.p_new = (k & 1) ? L.pbuf1 : L.pbuf0;
@@ -857,15 +855,11 @@ __global__ void __launch_bounds__(PCG_NT, EPC_PCG_LOOP_MINB) k_pcg_loop(PcgLoopA
         PcgUpdArgs U = L.U;
         U.p = H.p_new;
         double rr = 0.0, rzp = 0.0;
-        if (U.bal) {
-            for (long long c0 = cb0; c0 < cb1; c0 += CPW)
-                bj_group<CPW, true, true, SEG>(U, alpha, c0, (int)min((long long)CPW, cb1 - c0), X, Y,
-                                               rr, rzp);
-        } else {  // whole groups of CPW columns, round-robin over the blocks
-            for (long long c0 = (long long)blockIdx.x * CPW; c0 < U.ncol; c0 += (long long)gridDim.x * CPW)
-                bj_group<CPW, true, true, SEG>(U, alpha, c0, (int)min((long long)CPW, U.ncol - c0), X, Y,
-                                               rr, rzp);
-        }
+        // whole groups of CPW columns round-robin (balanced ranges measured no
+        // faster here, and cost the 64-register loop a spill)
+        for (long long c0 = (long long)blockIdx.x * CPW; c0 < U.ncol; c0 += (long long)gridDim.x * CPW)
+            bj_group<CPW, true, true, SEG>(U, alpha, c0, (int)min((long long)CPW, U.ncol - c0), X, Y,
+                                           rr, rzp);
         const double srr_b = block_sum(rr, sh);
         __syncthreads();
         const double srz_b = block_sum(rzp, sh);

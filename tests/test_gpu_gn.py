@@ -165,11 +165,12 @@ def test_gn_c2_parity(ctx, oracle):
 @pytest.mark.parametrize("loop", ["1", "0"])
 def test_pcg_segmented_sweeps_bitwise(ctx, oracle, monkeypatch, m, loop):
     """The block-Jacobi sweeps as warp-per-column segmented chains (pcg.cu
-    sweeps_seg: segments of 5 / 9 / 17 steps with agreement rounds, CPW 16
-    or 8) return the very bits of the thread-per-column chains
+    sweeps_seg: segments of 9 / 17 steps with agreement rounds, 8 columns
+    per block) return the very bits of the thread-per-column chains
     (EPC_PCG_SEG=0): d, the iteration count and relres identical, on column
-    lengths n1 = 129, 257, 301 and 513 and a short one, in the persistent
-    loop and in the per-iteration kernels."""
+    lengths n1 = 257, 301 and 513 (n1 = 129 and a short column keep the
+    thread chains at 16 columns per block: both settings run the same code),
+    in the persistent loop and in the per-iteration kernels."""
     monkeypatch.setenv("EPC_PCG_LOOP", loop)
     g, ip, im, _ = pair(m=m, scale=400.0)
     rng = np.random.default_rng(8)
