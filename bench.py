@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-f32", action="store_true", help="skip the fp32-variant leg")
     ap.add_argument("--no-gn-c3", action="store_true", help="skip the GN-PCG C3 leg")
     ap.add_argument("--no-x400", action="store_true", help="skip the amplitude-x400 C3 leg")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the C4 / C5 sharded legs even at one rank (they run by default at N > 1)")
     return ap.parse_args()
 
 
@@ -729,6 +731,72 @@ def run_slabs(a, iters):
     return 0
 
 
+def run_sharded_legs(a, ctx, dev, stream, dist, rank, world, iters=10):
+    """--gpus N > 1 (or --sharded): the configs that shard one workload over
+    the ranks, beside the C3 replicas, so a scaling run measures
+    communication:
+      C4: the 64 pairs in contiguous blocks per rank (epc_admm_solve_batch),
+          no collective; value = all pairs' face-iterations / max-over-ranks time;
+      C5: one 512x512x256 volume in k-slabs (dist_admm over NCCL): the time
+          of every collective kind (all-to-all transposes, halo, all-gather)
+          measured per rank (max over ranks), strong scaling.
+    `iters` ADMM iterations per solve (fixed count)."""
+    import torch
+    from paper_1607_00531_b200 import dist_admm, shard
+    cfg = abi.AdmmConfig(max_iter=iters, eps_abs=1e-300, eps_rel=1e-300)
+    out = {}
+    # C4
+    first, npairs = shard.shard_range(64, rank, world)
+    g4, ip4, im4 = synth.make_batch("C4", npairs=npairs, first=first)
+    ip4d, im4d = torch.from_numpy(ip4).to(dev), torch.from_numpy(im4).to(dev)
+    ctx.admm_solve_batch(g4, npairs, ip4d, im4d, cfg=abi.AdmmConfig(max_iter=1, eps_abs=1e-300, eps_rel=1e-300))
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ctx.admm_solve_batch(g4, npairs, ip4d, im4d, cfg=cfg)
+    e1.record(stream)
+    e1.synchronize()
+    t4 = shard.max_over_ranks(e0.elapsed_time(e1) / 1e3, dist, dev)
+    out["C4"] = {"workload": f"ADMM C4 64 x 128x128x64 pairs, {iters} iterations, pairs sharded over "
+                             f"{world} ranks", "value": g4.faces * 64 * iters / t4, "unit": UNIT,
+                 "seconds": t4, "scaling": "weak per pair, strong per batch", "collectives": {}}
+    del ip4d, im4d
+    # C5
+    d5 = synth.make_config("C5")
+    g5 = d5.grid
+    slabs = dist_admm.Slabs(g5.m[0], g5.m[1], g5.m[2], world)
+    k0, mk = slabs.k_range(rank)
+    cl = g5.m[0] * g5.m[1]
+    ip5 = torch.from_numpy(np.ascontiguousarray(d5.iplus[k0 * cl:(k0 + mk) * cl])).to(dev)
+    im5 = torch.from_numpy(np.ascontiguousarray(d5.iminus[k0 * cl:(k0 + mk) * cl])).to(dev)
+    del d5
+    backend = dist_admm.DeviceBackend(ctx, dev)
+
+    def solve(n, timings=None):
+        c = abi.AdmmConfig(max_iter=n, eps_abs=1e-300, eps_rel=1e-300)
+        gen = dist_admm.admm_rank(backend, g5, slabs, rank, ip5, im5, cfg=c)
+        return dist_admm.run_torch(gen, dist, dev, timings=timings)
+
+    solve(1)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    t0 = time.perf_counter()
+    solve(iters)
+    torch.cuda.synchronize(dev)
+    t5 = shard.max_over_ranks(time.perf_counter() - t0, dist, dev)
+    tim = {}
+    solve(iters, timings=tim)  # a second solve with every collective timed
+    coll = {k: {"seconds_per_iteration": shard.max_over_ranks(v[0], dist, dev) / iters,
+                "calls_per_iteration": v[1] / iters} for k, v in sorted(tim.items())}
+    out["C5"] = {"workload": f"ADMM C5 512x512x256, {iters} iterations, k-slabs over {world} ranks",
+                 "value": g5.faces * iters / t5, "unit": UNIT, "seconds": t5, "scaling": "strong",
+                 "collectives": coll,
+                 "note": "wall time (the slab driver synchronises between steps); collective times "
+                         "from a second, instrumented solve, max over ranks"}
+    return out
+
+
 def main():
     a = parse()
     iters = a.iters or DEFAULT_ITERS.get(a.config, 50)
@@ -914,7 +982,7 @@ def main():
             one = synth.VolumePairData(g, np.ascontiguousarray(ipn[:g.cells]),
                                        np.ascontiguousarray(imn[:g.cells]), None)
             cpu = cpu_windows_baseline(ctx, one, ip_d, im_d, iters, a.config,
-                                       starts=[int(iters * f) for f in (0, .2, .4, .6, .8)], n=2)
+                                       starts=[int(iters * f) for f in (0, .2, .4, .6, .8)], n=3)
         except Exception as e:  # the checker is optional on a bench box
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
                    "sample": str(e)[:120]}
@@ -927,6 +995,9 @@ def main():
                              min_solves=3)
     if a.config == "C3" and not a.no_x400 and a.scale == 1.0:
         x400 = run_x400_leg(a, ctx, dev, stream, flush, iters, rank, dist)
+    sharded = None
+    if a.config == "C3" and (world > 1 or a.sharded) and dist is not None:
+        sharded = run_sharded_legs(a, ctx, dev, stream, dist, rank, world)
     f32 = None
     if not a.no_f32 and a.config != "C4":
         f32 = run_f32_leg(a, ctx, dev, stream, flush, g, ipn, imn, iters, last_b, dist)
@@ -948,6 +1019,8 @@ def main():
             line["gn_c3"] = gn3
         if x400 is not None:
             line["x400"] = x400
+        if sharded is not None:
+            line["sharded"] = sharded
         if f32 is not None:
             line["fp32"] = f32
         print(json.dumps(line), flush=True)

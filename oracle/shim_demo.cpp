@@ -67,7 +67,10 @@ int main(int argc, char** argv) {
     put(f, meta);
     // the GN building blocks (objective_gn, GnHessian, make_preconditioner)
     // driven through the reference's own generic pcg (gn_pcg.cpp:92-131)
-    const StaggeredField& bq = gsol.b;  // a feasible, nonzero field
+    // a feasible, nonzero field that both builds hold bitwise (the ADMM
+    // result is bitwise; halving it is exact and keeps |D1 b| < 1)
+    StaggeredField bq = a.state.b;
+    for (double& v : bq.v) v *= 0.5;
     const ObjectiveEval ev = objective_gn(pair, bq, p);
     put(f, ev.grad.v);
     put(f, ev.residual.v);

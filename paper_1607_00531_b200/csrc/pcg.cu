@@ -480,7 +480,7 @@ __device__ __forceinline__ void sweeps_thread(const PcgUpdArgs& A, int nc, doubl
     }
     __syncthreads();
 #pragma unroll 2
-    for (int h = tid; h < ne2; h += PCG_NT) {
+    for (int h = tid; h < ne2; h += (int)blockDim.x) {
         const double2 dd = __ldg(reinterpret_cast<const double2*>(FD + base + 2 * (size_t)h));
         const int k0 = sidx(2 * h), k1 = sidx(2 * h + 1);
         X[k0] = X[k0] / dd.x;
@@ -551,7 +551,7 @@ __device__ __forceinline__ void sweeps_seg(const PcgUpdArgs& A, int nc, double* 
     const int tid = threadIdx.x, lane = tid & 31, n1 = A.n1, RS = A.tile_rs;
     double* const T = const_cast<double*>(Y) + CPW * RS;  // third staged array
     const double* __restrict__ FD = A.fd;
-    for (int cc = tid >> 5; cc < nc; cc += PCG_NT / 32) {
+    for (int cc = tid >> 5; cc < nc; cc += (int)(blockDim.x >> 5)) {
         const double* x = X + cc * RS;
         double* t = T + cc * RS;
         const double* y = Y + cc * RS;
@@ -566,7 +566,7 @@ __device__ __forceinline__ void sweeps_seg(const PcgUpdArgs& A, int nc, double* 
     }
     __syncthreads();
 #pragma unroll 2
-    for (int h = tid; h < ne2; h += PCG_NT) {
+    for (int h = tid; h < ne2; h += (int)blockDim.x) {
         const double2 dd = __ldg(reinterpret_cast<const double2*>(FD + base + 2 * (size_t)h));
         const int k0 = sidx(2 * h), k1 = sidx(2 * h + 1);
         T[k0] = T[k0] / dd.x;
@@ -577,7 +577,7 @@ __device__ __forceinline__ void sweeps_seg(const PcgUpdArgs& A, int nc, double* 
         T[k] = T[k] / __ldg(FD + base + ne - 1);
     }
     __syncthreads();
-    for (int cc = tid >> 5; cc < nc; cc += PCG_NT / 32) {
+    for (int cc = tid >> 5; cc < nc; cc += (int)(blockDim.x >> 5)) {
         double* x = X + cc * RS;
         const double* t = T + cc * RS;
         const double* y = Y + cc * RS;
@@ -648,7 +648,7 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
     // / r stores itself). The loop kernel (64-register cap) keeps the lean form.
     if constexpr (COH) {
 #pragma unroll 2
-        for (int h = tid; h < ne2; h += PCG_NT) {
+        for (int h = tid; h < ne2; h += (int)blockDim.x) {
             const size_t o = base + 2 * (size_t)h;
             double2 r = *reinterpret_cast<const double2*>(Rv + o);
             const double2 pp = ld_vec2<COH>(Pv + o), qq = ld_vec2<COH>(Qv + o);
@@ -663,11 +663,11 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
             stage1(2 * h, r.x, l.x);
             stage1(2 * h + 1, r.y, l.y);
         }
-    } else for (int h0 = tid; h0 < ne2; h0 += 2 * PCG_NT) {
+    } else for (int h0 = tid; h0 < ne2; h0 += 2 * (int)blockDim.x) {
         double2 r[2], pp[2], qq[2], dd[2], l[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const int h = min(h0 + u * PCG_NT, ne2 - 1);
+            const int h = min(h0 + u * (int)blockDim.x, ne2 - 1);
             const size_t o = base + 2 * (size_t)h;
             r[u] = *reinterpret_cast<const double2*>(Rv + o);
             if (UPD) {
@@ -679,7 +679,7 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const int h = h0 + u * PCG_NT;
+            const int h = h0 + u * (int)blockDim.x;
             if (h >= ne2) break;
             const size_t o = base + 2 * (size_t)h;
             if (UPD) {
@@ -710,7 +710,7 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
     else sweeps_thread(A, nc, X, Y, base, sidx, ne, ne2);
     if constexpr (COH) {
 #pragma unroll 2
-        for (int h = tid; h < ne2; h += PCG_NT) {
+        for (int h = tid; h < ne2; h += (int)blockDim.x) {
             const size_t o = base + 2 * (size_t)h;
             const double2 r = *reinterpret_cast<const double2*>(Rv + o);
             const double2 z = make_double2(X[sidx(2 * h)], X[sidx(2 * h + 1)]);
@@ -718,14 +718,14 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
             rz += r.x * z.x;
             rz += r.y * z.y;
         }
-    } else for (int h0 = tid; h0 < ne2; h0 += 2 * PCG_NT) {  // loads of both pairs first
+    } else for (int h0 = tid; h0 < ne2; h0 += 2 * (int)blockDim.x) {  // loads of both pairs first
         double2 r[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u)
-            r[u] = *reinterpret_cast<const double2*>(Rv + base + 2 * (size_t)min(h0 + u * PCG_NT, ne2 - 1));
+            r[u] = *reinterpret_cast<const double2*>(Rv + base + 2 * (size_t)min(h0 + u * (int)blockDim.x, ne2 - 1));
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const int h = h0 + u * PCG_NT;
+            const int h = h0 + u * (int)blockDim.x;
             if (h >= ne2) break;
             const double2 z = make_double2(X[sidx(2 * h)], X[sidx(2 * h + 1)]);
             *reinterpret_cast<double2*>(Zv + base + 2 * (size_t)h) = z;
@@ -742,8 +742,11 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
     __syncthreads();
 }
 
+// 4 columns per block run as 128-thread blocks (a warp per column in the sweeps)
+template <int CPW> constexpr int bj_threads() { return CPW == 4 ? 128 : PCG_NT; }
+
 template <int CPW, bool UPD, int SEG>
-__global__ void __launch_bounds__(PCG_NT) k_pcg_update_bj(PcgUpdArgs A, PcgState* S) {
+__global__ void __launch_bounds__(bj_threads<CPW>()) k_pcg_update_bj(PcgUpdArgs A, PcgState* S) {
     extern __shared__ __align__(16) double usm[];
     __shared__ double sh[8];
     if (S->done) return;
@@ -901,7 +904,7 @@ __global__ void __launch_bounds__(PCG_NT, EPC_PCG_LOOP_MINB) k_pcg_loop(PcgLoopA
 // Cooperative launch of the loop; false when the device cannot hold the grid.
 // (CPW, SEG) instantiations: 16 columns per block (n1 <= ~160) keep the
 // thread chains; 8 for longer columns, segments 9 or 17
-#define PCG_VARIANTS(X) X(16, 0) X(8, 0) X(8, 9) X(8, 17)
+#define PCG_VARIANTS(X) X(16, 0) X(8, 0) X(8, 9) X(8, 17) X(4, 9) X(4, 17)
 
 static const void* pcg_loop_fn(int cpw, int seg) {
 #define PCG_PICK(C, S) if (cpw == C && seg == S) return (const void*)k_pcg_loop<C, S>;
@@ -942,8 +945,8 @@ void launch_pcg_update_bj(epc_context* ctx, int cpw, int seg, int blocks, size_t
     const bool upd = U.phase == 1;
 #define PCG_LAUNCH_UPD(C, SG)                                                                       \
     if (cpw == C && seg == SG) {                                                                   \
-        if (upd) EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<C, true, SG>), blocks, PCG_NT, smem, U, S); \
-        else EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<C, false, SG>), blocks, PCG_NT, smem, U, S); \
+        if (upd) EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<C, true, SG>), blocks, bj_threads<C>(), smem, U, S); \
+        else EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<C, false, SG>), blocks, bj_threads<C>(), smem, U, S); \
         return;                                                                                    \
     }
     PCG_VARIANTS(PCG_LAUNCH_UPD)
@@ -955,7 +958,7 @@ int pcg_update_bj_per_sm(int cpw, int seg, size_t smem) {
     int per = 0;
 #define PCG_OCC(C, SG)                                                                      \
     if (cpw == C && seg == SG)                                                              \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_update_bj<C, true, SG>, PCG_NT, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_update_bj<C, true, SG>, bj_threads<C>(), smem);
     PCG_VARIANTS(PCG_OCC)
 #undef PCG_OCC
     return per > 0 ? per : 1;

@@ -264,16 +264,25 @@ def run_lockstep(gens, cat, split):
         reqs = nxt
 
 
-def run_torch(gen, dist, device):
+def run_torch(gen, dist, device, timings=None):
     """Run this rank's generator with torch.distributed collectives
-    (NCCL for CUDA tensors, gloo for CPU tensors)."""
+    (NCCL for CUDA tensors, gloo for CPU tensors). timings: optional dict,
+    accumulates seconds and counts per collective kind (each collective is
+    then bracketed by device synchronisations)."""
+    import time as _time
+
     import torch
     rank, world = dist.get_rank(), dist.get_world_size()
     as_t = _as_tensor
+    cuda = isinstance(device, torch.device) and device.type == "cuda"
     try:
         req = next(gen)
         while True:
             kind = req[0]
+            if timings is not None:
+                if cuda:
+                    torch.cuda.synchronize(device)
+                t_req = _time.perf_counter()
             if kind == "alltoall":
                 _, send, scounts, recv, rcounts = req
                 ts, tr = as_t(send), as_t(recv)
@@ -323,6 +332,12 @@ def run_torch(gen, dist, device):
                 ans = t.cpu().tolist()
             else:
                 raise RuntimeError(kind)
+            if timings is not None:
+                if cuda:
+                    torch.cuda.synchronize(device)
+                tk = timings.setdefault(kind, [0.0, 0])
+                tk[0] += _time.perf_counter() - t_req
+                tk[1] += 1
             req = gen.send(ans)
     except StopIteration as e:
         return e.value
