@@ -742,8 +742,9 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
     __syncthreads();
 }
 
-// 4 columns per block run as 128-thread blocks (a warp per column in the sweeps)
-template <int CPW> constexpr int bj_threads() { return CPW == 4 ? 128 : PCG_NT; }
+// threads per block of the per-iteration update (4 columns per 128-thread
+// block measured within 2% of 8 per 256 at C3: not kept)
+template <int CPW> constexpr int bj_threads() { return PCG_NT; }
 
 template <int CPW, bool UPD, int SEG>
 __global__ void __launch_bounds__(bj_threads<CPW>()) k_pcg_update_bj(PcgUpdArgs A, PcgState* S) {
@@ -904,7 +905,7 @@ __global__ void __launch_bounds__(PCG_NT, EPC_PCG_LOOP_MINB) k_pcg_loop(PcgLoopA
 // Cooperative launch of the loop; false when the device cannot hold the grid.
 // (CPW, SEG) instantiations: 16 columns per block (n1 <= ~160) keep the
 // thread chains; 8 for longer columns, segments 9 or 17
-#define PCG_VARIANTS(X) X(16, 0) X(8, 0) X(8, 9) X(8, 17) X(4, 9) X(4, 17)
+#define PCG_VARIANTS(X) X(16, 0) X(8, 0) X(8, 9) X(8, 17)
 
 static const void* pcg_loop_fn(int cpw, int seg) {
 #define PCG_PICK(C, S) if (cpw == C && seg == S) return (const void*)k_pcg_loop<C, S>;
