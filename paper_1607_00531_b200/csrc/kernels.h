@@ -202,11 +202,13 @@ struct PcgUpdArgs {
 __global__ void k_pcg_start(const double* g, double* r, double* d, long long n, double* partials,
                             PcgState* S);
 __global__ void k_pcg_hvp(PcgHvArgs A, PcgState* S);
-void launch_pcg_update_bj(epc_context* ctx, int cpw, int seg, int blocks, size_t smem, const PcgUpdArgs& U,
-                          PcgState* S);
-void set_pcg_update_bj_smem(int cpw, int seg, int bytes);
+// ws: the warp-specialised pipelined kernel (k_pcg_update_ws; pcg_ws_ok)
+void launch_pcg_update_bj(epc_context* ctx, int cpw, int seg, bool ws, int blocks, size_t smem,
+                          const PcgUpdArgs& U, PcgState* S);
+void set_pcg_update_bj_smem(int cpw, int seg, bool ws, int bytes);
 bool pcg_variant_ok(int cpw, int seg);
-int pcg_update_bj_per_sm(int cpw, int seg, size_t smem);  // after set_pcg_update_bj_smem
+bool pcg_ws_ok(int cpw, int seg);
+int pcg_update_bj_per_sm(int cpw, int seg, bool ws, size_t smem);  // after set_pcg_update_bj_smem
 int pcg_hvp_per_sm();  // an instantiated (columns per block, segment) pair
 struct PcgLoopArgs {
     PcgHvArgs H;

@@ -515,7 +515,10 @@ __device__ __forceinline__ void sweeps_thread(const PcgUpdArgs& A, int nc, doubl
 // a lane's guess is never overwritten under it; after SEG_ROUNDS rounds lane
 // 0 runs the one-thread chain instead.
 constexpr int PCG_SEG_ROUNDS = 8;
-template <int S, bool BWD>
+#ifndef EPC_PCG_UMULHI
+#define EPC_PCG_UMULHI 1
+#endif
+template <int S, bool BWD, bool PIPE>
 __device__ __forceinline__ bool pcg_seg_sweep(const double* __restrict__ src,
                                               double* __restrict__ dst,
                                               const double* __restrict__ l, int n) {
@@ -530,10 +533,27 @@ __device__ __forceinline__ bool pcg_seg_sweep(const double* __restrict__ src,
     for (int round = 0; round < PCG_SEG_ROUNDS; ++round) {
         double p = st;
         int e = e0;
+        if constexpr (PIPE) {
+            // the next step's operands loaded while this step runs (index
+            // clamped into the column), so no shared-memory round trip sits
+            // on the chain
+            double sv = src[e], lv = l[BWD ? e : e - 1];
 #pragma unroll 1
-        for (int j = 0; j < cnt; ++j, e += BWD ? -1 : 1) {
-            p = src[e] - l[BWD ? e : e - 1] * p;
-            dst[e] = p;
+            for (int j = 0; j < cnt; ++j) {
+                const int en = BWD ? max(e - 1, 0) : min(e + 1, n - 1);
+                const double sn = src[en], ln = l[BWD ? en : en - 1];
+                p = sv - lv * p;
+                dst[e] = p;
+                sv = sn;
+                lv = ln;
+                e = en;
+            }
+        } else {
+#pragma unroll 1
+            for (int j = 0; j < cnt; ++j, e += BWD ? -1 : 1) {
+                p = src[e] - l[BWD ? e : e - 1] * p;
+                dst[e] = p;
+            }
         }
         const double end = cnt > 0 ? p : st;
         const double pe = __shfl_up_sync(FULL_MASK, end, 1);
@@ -555,7 +575,7 @@ __device__ __forceinline__ void sweeps_seg(const PcgUpdArgs& A, int nc, double* 
         const double* x = X + cc * RS;
         double* t = T + cc * RS;
         const double* y = Y + cc * RS;
-        if (!pcg_seg_sweep<S, false>(x, t, y, n1) && lane == 0) {
+        if (!pcg_seg_sweep<S, false, false>(x, t, y, n1) && lane == 0) {
             double prev = x[0];
             t[0] = prev;
             for (int i = 1; i < n1; ++i) {
@@ -581,7 +601,7 @@ __device__ __forceinline__ void sweeps_seg(const PcgUpdArgs& A, int nc, double* 
         double* x = X + cc * RS;
         const double* t = T + cc * RS;
         const double* y = Y + cc * RS;
-        if (!pcg_seg_sweep<S, true>(t, x, y, n1) && lane == 0) {
+        if (!pcg_seg_sweep<S, true, false>(t, x, y, n1) && lane == 0) {
             double nxt = t[n1 - 1];
             x[n1 - 1] = nxt;
             for (int i = n1 - 2; i >= 0; --i) {
@@ -628,15 +648,24 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
     double* __restrict__ Zv = A.z;
     const double* __restrict__ Pv = A.p;
     const double* __restrict__ Qv = A.q;
-    const double* __restrict__ FD = A.fd;
     const double* __restrict__ FL = A.fl;
     const size_t base = (size_t)c0 * n1;
     const int ne = nc * n1;
     const int ne2 = ne >> 1;
+#if EPC_PCG_UMULHI
+    // e / n1 as a multiply-high by ceil(2^32 / n1): exact for e < 2^32 / n1
+    // (a group spans CPW n1 faces)
+    const unsigned mg = 0xffffffffu / un1 + 1u;
+    auto sidx = [&](int e) {
+        const int cc = (int)__umulhi((unsigned)e, mg);
+        return cc * RS + (e - cc * n1);
+    };
+#else
     auto sidx = [&](int e) {
         const int cc = (int)((unsigned)e / un1);
         return cc * RS + (e - cc * n1);
     };
+#endif
     auto stage1 = [&](int e, double r0, double l0) {
         rr += r0 * r0;
         const int k = sidx(e);
@@ -665,6 +694,18 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
         }
     } else for (int h0 = tid; h0 < ne2; h0 += 2 * (int)blockDim.x) {
         double2 r[2], pp[2], qq[2], dd[2], l[2];
+#if EPC_PCG_EXP == 2  // timing experiment: no global traffic
+        if (true) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int h = h0 + u * (int)blockDim.x;
+                if (h >= ne2) break;
+                stage1(2 * h, 1.0 + a * h, 0.25);
+                stage1(2 * h + 1, 1.0 - a * h, 0.25);
+            }
+            continue;
+        }
+#endif
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int h = min(h0 + u * (int)blockDim.x, ne2 - 1);
@@ -706,8 +747,13 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
         stage1(ne - 1, r, __ldg(FL + o));
     }
     __syncthreads();
-    if (SEG) sweeps_seg<SEG, CPW>(A, nc, X, Y, base, sidx, ne, ne2);
+#if EPC_PCG_EXP == 1  // timing experiment: no sweeps
+    if (COH)
+#endif
+    {
+    if constexpr (SEG != 0) sweeps_seg<SEG, CPW>(A, nc, X, Y, base, sidx, ne, ne2);
     else sweeps_thread(A, nc, X, Y, base, sidx, ne, ne2);
+    }
     if constexpr (COH) {
 #pragma unroll 2
         for (int h = tid; h < ne2; h += (int)blockDim.x) {
@@ -720,6 +766,16 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
         }
     } else for (int h0 = tid; h0 < ne2; h0 += 2 * (int)blockDim.x) {  // loads of both pairs first
         double2 r[2];
+#if EPC_PCG_EXP == 2
+        if (true) {
+            for (int u = 0; u < 2; ++u) {
+                const int h = h0 + u * (int)blockDim.x;
+                if (h >= ne2) break;
+                rz += X[sidx(2 * h)] + X[sidx(2 * h + 1)];
+            }
+            continue;
+        }
+#endif
 #pragma unroll
         for (int u = 0; u < 2; ++u)
             r[u] = *reinterpret_cast<const double2*>(Rv + base + 2 * (size_t)min(h0 + u * (int)blockDim.x, ne2 - 1));
@@ -747,7 +803,10 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
 template <int CPW> constexpr int bj_threads() { return PCG_NT; }
 
 template <int CPW, bool UPD, int SEG>
-__global__ void __launch_bounds__(bj_threads<CPW>()) k_pcg_update_bj(PcgUpdArgs A, PcgState* S) {
+#ifndef EPC_PCG_BJ_MINB
+#define EPC_PCG_BJ_MINB 4  // shared memory holds 4 blocks per SM at C3 (n1 = 257): keep 64 registers
+#endif
+__global__ void __launch_bounds__(bj_threads<CPW>(), EPC_PCG_BJ_MINB) k_pcg_update_bj(PcgUpdArgs A, PcgState* S) {
     extern __shared__ __align__(16) double usm[];
     __shared__ double sh[8];
     if (S->done) return;
@@ -759,6 +818,238 @@ __global__ void __launch_bounds__(bj_threads<CPW>()) k_pcg_update_bj(PcgUpdArgs 
     block_columns(A.ncol, cb0, cb1);
     for (long long c0 = cb0; c0 < cb1; c0 += CPW)
         bj_group<CPW, UPD, false, SEG>(A, a, c0, (int)min((long long)CPW, cb1 - c0), X, Y, rr, rz);
+    const double srr_b = block_sum(rr, sh);
+    __syncthreads();
+    const double srz_b = block_sum(rz, sh);
+    if (threadIdx.x == 0) {
+        A.partials[(size_t)blockIdx.x * 2 + 0] = srr_b;
+        A.partials[(size_t)blockIdx.x * 2 + 1] = srz_b;
+    }
+    if (arrive_last(&S->cnt)) {
+        __syncthreads();
+        const double srr = last_block_sum(A.partials, gridDim.x, 2, 0, sh);
+        __syncthreads();
+        const double srz = last_block_sum(A.partials, gridDim.x, 2, 1, sh);
+        if (threadIdx.x == 0) pcg_finish(S, A.phase, srr, srz);
+    }
+}
+
+// ---- block-Jacobi update, warp-specialised and pipelined ---------------------
+// The same five steps, with the memory passes and the sweeps of different
+// column groups in flight at once. A block of 2 x PCG_NT threads: the first
+// PCG_NT (the "memory" warps) run steps 1 and 5, the second PCG_NT (one
+// "sweep" warp per column) steps 2-4, over two shared-memory stages. While
+// the sweep warps solve group g in one stage, the memory warps finish group
+// g-1 (z written, r.z) and stage group g+1 in the other, so HBM is busy
+// during the serial chains instead of idling behind a block barrier (the
+// single-role kernel's blocks on an SM start together and stay in step).
+// Named barriers hand a stage over: FULL (memory -> sweep), SWEPT (sweep ->
+// memory). Each column's sweeps are the same operations on the same operands
+// as k_pcg_update_bj's, so z is bitwise the same; the r.r / r.z partials
+// follow this kernel's own fixed thread mapping.
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+enum { WS_FULL = 1, WS_SWEPT = 3, WS_MEM = 5 };  // FULL / SWEPT: + stage (0, 1)
+
+// step 1 for one group by the memory warps (thread t of PCG_NT): d += a p,
+// r += (-a) q written back, r and l staged; accumulates r.r
+template <bool UPD, class SIDX>
+__device__ __forceinline__ void ws_stage(const PcgUpdArgs& A, double a, size_t base, int ne,
+                                         double* X, double* Y, const SIDX& sidx, int t, double& rr) {
+    const double ma = -a;
+    double* __restrict__ Dv = A.d;
+    double* __restrict__ Rv = A.r;
+    const double* __restrict__ Pv = A.p;
+    const double* __restrict__ Qv = A.q;
+    const double* __restrict__ FL = A.fl;
+    const int ne2 = ne >> 1;
+    auto put = [&](int e, double r0, double l0) {
+        rr += r0 * r0;
+        const int k = sidx(e);
+        X[k] = r0;
+        Y[k] = l0;
+    };
+    for (int h0 = t; h0 < ne2; h0 += 2 * PCG_NT) {
+        double2 r[2], pp[2], qq[2], dd[2], l[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int h = min(h0 + u * PCG_NT, ne2 - 1);
+            const size_t o = base + 2 * (size_t)h;
+            r[u] = *reinterpret_cast<const double2*>(Rv + o);
+            if (UPD) {
+                pp[u] = __ldg(reinterpret_cast<const double2*>(Pv + o));
+                qq[u] = __ldg(reinterpret_cast<const double2*>(Qv + o));
+                dd[u] = *reinterpret_cast<const double2*>(Dv + o);
+            }
+            l[u] = __ldg(reinterpret_cast<const double2*>(FL + o));
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int h = h0 + u * PCG_NT;
+            if (h >= ne2) break;
+            const size_t o = base + 2 * (size_t)h;
+            if (UPD) {
+                dd[u].x = dd[u].x + a * pp[u].x;
+                dd[u].y = dd[u].y + a * pp[u].y;
+                r[u].x += ma * qq[u].x;
+                r[u].y += ma * qq[u].y;
+                *reinterpret_cast<double2*>(Dv + o) = dd[u];
+                *reinterpret_cast<double2*>(Rv + o) = r[u];
+            }
+            put(2 * h, r[u].x, l[u].x);
+            put(2 * h + 1, r[u].y, l[u].y);
+        }
+    }
+    if ((ne & 1) && t == 0) {
+        const size_t o = base + ne - 1;
+        double r = Rv[o];
+        if (UPD) {
+            const double dn = Dv[o] + a * __ldg(Pv + o);
+            r += ma * __ldg(Qv + o);
+            Dv[o] = dn;
+            Rv[o] = r;
+        }
+        put(ne - 1, r, __ldg(FL + o));
+    }
+}
+
+// step 5 for one group by the memory warps: z written, r.z accumulated
+template <class SIDX>
+__device__ __forceinline__ void ws_final(const PcgUpdArgs& A, size_t base, int ne, const double* X,
+                                         const SIDX& sidx, int t, double& rz) {
+    double* __restrict__ Zv = A.z;
+    const double* __restrict__ Rv = A.r;
+    const int ne2 = ne >> 1;
+    for (int h0 = t; h0 < ne2; h0 += 2 * PCG_NT) {
+        double2 r[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            r[u] = *reinterpret_cast<const double2*>(Rv + base + 2 * (size_t)min(h0 + u * PCG_NT, ne2 - 1));
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int h = h0 + u * PCG_NT;
+            if (h >= ne2) break;
+            const double2 z = make_double2(X[sidx(2 * h)], X[sidx(2 * h + 1)]);
+            *reinterpret_cast<double2*>(Zv + base + 2 * (size_t)h) = z;
+            rz += r[u].x * z.x;
+            rz += r[u].y * z.y;
+        }
+    }
+    if ((ne & 1) && t == 0) {
+        const size_t o = base + ne - 1;
+        const double zz = X[sidx(ne - 1)];
+        Zv[o] = zz;
+        rz += Rv[o] * zz;
+    }
+}
+
+// steps 2-4 for one column by its sweep warp: forward sweep, divisions by
+// d, backward sweep (segmented chains, or lane 0's chain when SEG = 0)
+#ifndef EPC_PCG_WS_PIPE
+#define EPC_PCG_WS_PIPE 1
+#endif
+template <int SEG>
+__device__ __forceinline__ void ws_sweep_column(double* x, double* t, const double* y,
+                                                const double* __restrict__ fd, int n1) {
+    const int lane = threadIdx.x & 31;
+    constexpr bool WS_PIPE = EPC_PCG_WS_PIPE;
+    if constexpr (SEG == 0) {
+        ldlt_solve_warp(x, y, fd, n1);
+        (void)t;
+    } else {
+        // the divisors of the lane's forward segment, loaded ahead of the
+        // forward chain (their HBM latency hidden behind it)
+        const int r0 = 1 + lane * SEG;
+        const int cnt = max(0, min(SEG, n1 - r0));
+        double dv[SEG];
+#pragma unroll
+        for (int j = 0; j < SEG; ++j) dv[j] = __ldg(fd + min(r0 + j, n1 - 1));
+        const double d0 = __ldg(fd);
+        if (!pcg_seg_sweep<SEG, false, WS_PIPE>(x, t, y, n1) && lane == 0) {
+            double prev = x[0];
+            t[0] = prev;
+            for (int i = 1; i < n1; ++i) {
+                prev = x[i] - y[i - 1] * prev;
+                t[i] = prev;
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < SEG; ++j)
+            if (j < cnt) t[r0 + j] = t[r0 + j] / dv[j];
+        if (lane == 0) t[0] = t[0] / d0;
+        __syncwarp();
+        if (!pcg_seg_sweep<SEG, true, WS_PIPE>(t, x, y, n1) && lane == 0) {
+            double nxt = t[n1 - 1];
+            x[n1 - 1] = nxt;
+            for (int i = n1 - 2; i >= 0; --i) {
+                nxt = t[i] - y[i] * nxt;
+                x[i] = nxt;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <int CPW, bool UPD, int SEG>
+__global__ void __launch_bounds__(2 * PCG_NT, 2) k_pcg_update_ws(PcgUpdArgs A, PcgState* S) {
+    static_assert(CPW * 32 <= PCG_NT, "one sweep warp per column");
+    extern __shared__ __align__(16) double usm[];
+    __shared__ double sh[2 * PCG_NT / 32];
+    if (S->done) return;
+    const int n1 = A.n1, RS = A.tile_rs;
+    const unsigned un1 = (unsigned)n1;
+    const size_t stage_elems = (size_t)3 * CPW * RS;
+    const double a = S->alpha;
+    long long cb0, cb1;
+    block_columns(A.ncol, cb0, cb1);
+    const int G = (int)((cb1 - cb0 + CPW - 1) / CPW);
+    const unsigned mg = 0xffffffffu / un1 + 1u;  // e / n1 = umulhi(e, mg) for e < 2^32 / n1
+    auto sidx = [&](int e) {
+        const int cc = (int)__umulhi((unsigned)e, mg);
+        return cc * RS + (e - cc * n1);
+    };
+    constexpr int NB = 2 * PCG_NT;
+    double rr = 0.0, rz = 0.0;
+    if (threadIdx.x < PCG_NT) {  // memory warps
+        const int t = threadIdx.x;
+        auto stage = [&](int g) {
+            double* X = usm + (g & 1) * stage_elems;
+            const long long c0 = cb0 + (long long)g * CPW;
+            const int nc = (int)min((long long)CPW, cb1 - c0);
+            ws_stage<UPD>(A, a, (size_t)c0 * n1, nc * n1, X, X + CPW * RS, sidx, t, rr);
+            named_arrive(WS_FULL + (g & 1), NB);
+        };
+        for (int g = 0; g < min(G, 2); ++g) stage(g);
+        for (int g = 0; g < G; ++g) {
+            named_sync(WS_SWEPT + (g & 1), NB);
+            const long long c0 = cb0 + (long long)g * CPW;
+            const int nc = (int)min((long long)CPW, cb1 - c0);
+            ws_final(A, (size_t)c0 * n1, nc * n1, usm + (g & 1) * stage_elems, sidx, t, rz);
+            if (g + 2 < G) {
+                named_sync(WS_MEM, PCG_NT);  // every z read from the stage before it is refilled
+                stage(g + 2);
+            }
+        }
+    } else {  // sweep warps: warp w solves column w of each group
+        const int w = (threadIdx.x - PCG_NT) >> 5;
+        for (int g = 0; g < G; ++g) {
+            named_sync(WS_FULL + (g & 1), NB);
+            const long long c0 = cb0 + (long long)g * CPW;
+            const int nc = (int)min((long long)CPW, cb1 - c0);
+            if (w < nc) {
+                double* X = usm + (g & 1) * stage_elems;
+                ws_sweep_column<SEG>(X + w * RS, X + 2 * CPW * RS + w * RS, X + CPW * RS + w * RS,
+                                     A.fd + (size_t)(c0 + w) * n1, n1);
+            }
+            named_arrive(WS_SWEPT + (g & 1), NB);
+        }
+    }
+    __syncthreads();
     const double srr_b = block_sum(rr, sh);
     __syncthreads();
     const double srz_b = block_sum(rz, sh);
@@ -941,9 +1232,29 @@ bool launch_pcg_loop(epc_context* ctx, int cpw, int seg, size_t smem, const PcgL
     return e == cudaSuccess;
 }
 
-void launch_pcg_update_bj(epc_context* ctx, int cpw, int seg, int blocks, size_t smem,
+// the warp-specialised kernel's instantiations (8 columns per group)
+#define PCG_WS_VARIANTS(X) X(8, 0) X(8, 9) X(8, 17)
+
+bool pcg_ws_ok(int cpw, int seg) {
+#define PCG_WS_HAS(C, SG) if (cpw == C && seg == SG) return true;
+    PCG_WS_VARIANTS(PCG_WS_HAS)
+#undef PCG_WS_HAS
+    return false;
+}
+
+void launch_pcg_update_bj(epc_context* ctx, int cpw, int seg, bool ws, int blocks, size_t smem,
                           const PcgUpdArgs& U, PcgState* S) {
     const bool upd = U.phase == 1;
+    if (ws) {
+#define PCG_LAUNCH_WS(C, SG)                                                                        \
+    if (cpw == C && seg == SG) {                                                                   \
+        if (upd) EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_ws<C, true, SG>), blocks, 2 * PCG_NT, smem, U, S); \
+        else EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_ws<C, false, SG>), blocks, 2 * PCG_NT, smem, U, S); \
+        return;                                                                                    \
+    }
+        PCG_WS_VARIANTS(PCG_LAUNCH_WS)
+#undef PCG_LAUNCH_WS
+    }
 #define PCG_LAUNCH_UPD(C, SG)                                                                       \
     if (cpw == C && seg == SG) {                                                                   \
         if (upd) EPC_LAUNCH(ctx, "pcg_update", (k_pcg_update_bj<C, true, SG>), blocks, bj_threads<C>(), smem, U, S); \
@@ -955,8 +1266,16 @@ void launch_pcg_update_bj(epc_context* ctx, int cpw, int seg, int blocks, size_t
 }
 
 // resident blocks per SM of the per-iteration kernels (grids sized to one wave)
-int pcg_update_bj_per_sm(int cpw, int seg, size_t smem) {
+int pcg_update_bj_per_sm(int cpw, int seg, bool ws, size_t smem) {
     int per = 0;
+    if (ws) {
+#define PCG_WS_OCC(C, SG)                                                                   \
+    if (cpw == C && seg == SG)                                                              \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_update_ws<C, true, SG>, 2 * PCG_NT, smem);
+        PCG_WS_VARIANTS(PCG_WS_OCC)
+#undef PCG_WS_OCC
+        return per > 0 ? per : 1;
+    }
 #define PCG_OCC(C, SG)                                                                      \
     if (cpw == C && seg == SG)                                                              \
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_update_bj<C, true, SG>, bj_threads<C>(), smem);
@@ -970,8 +1289,18 @@ int pcg_hvp_per_sm() {
     return per > 0 ? per : 1;
 }
 
-void set_pcg_update_bj_smem(int cpw, int seg, int bytes) {
+void set_pcg_update_bj_smem(int cpw, int seg, bool ws, int bytes) {
     const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    if (ws) {
+#define PCG_WS_SET(C, SG)                                                       \
+    if (cpw == C && seg == SG) {                                               \
+        cudaFuncSetAttribute(k_pcg_update_ws<C, true, SG>, attr, bytes);        \
+        cudaFuncSetAttribute(k_pcg_update_ws<C, false, SG>, attr, bytes);       \
+    }
+        PCG_WS_VARIANTS(PCG_WS_SET)
+#undef PCG_WS_SET
+        return;
+    }
 #define PCG_SET_SMEM(C, SG)                                                     \
     if (cpw == C && seg == SG) {                                               \
         cudaFuncSetAttribute(k_pcg_update_bj<C, true, SG>, attr, bytes);        \

@@ -30,4 +30,6 @@ with ThreadPoolExecutor(len(B.SOURCES)) as ex:
     objs = list(ex.map(cc, B.SOURCES))
 lib = os.path.join(out, f"{name}.so")
 subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", lib, *objs, *B.LIBS], check=True)
+for o in objs:  # keep only the library (the snapshot travels to the GPU box)
+    os.remove(o)
 print(lib)
