@@ -518,7 +518,7 @@ constexpr int PCG_SEG_ROUNDS = 8;
 #ifndef EPC_PCG_UMULHI
 #define EPC_PCG_UMULHI 1
 #endif
-template <int S, bool BWD, bool PIPE>
+template <int S, bool BWD, bool PIPE, int W = 0>
 __device__ __forceinline__ bool pcg_seg_sweep(const double* __restrict__ src,
                                               double* __restrict__ dst,
                                               const double* __restrict__ l, int n) {
@@ -527,6 +527,29 @@ __device__ __forceinline__ bool pcg_seg_sweep(const double* __restrict__ src,
     const int cnt = max(0, min(S, n - r0));
     if (lane == 0) dst[BWD ? n - 1 : 0] = src[BWD ? n - 1 : 0];
     double st = src[BWD ? n - min(r0, n) : min(r0, n) - 1];
+    if constexpr (W > 0) {
+        // warm-up: the start guess is the chain run over the W elements
+        // before the segment (nothing stored), from that element's own
+        // value; a wrong start decays like prod |l|, so the first round's
+        // guesses are already the chain's bits when W covers that decay
+        // (C3: one round instead of four). Only the speed depends on W --
+        // the rounds below still verify every start.
+        if (cnt > 0) {
+            if (BWD) {
+                int e = min(n - r0 + W, n - 1);
+                double p = src[e];
+#pragma unroll 1
+                for (--e; e >= n - r0; --e) p = src[e] - l[e] * p;
+                st = p;
+            } else {
+                int e = max(r0 - 1 - W, 0);
+                double p = src[e];
+#pragma unroll 1
+                for (++e; e <= r0 - 1; ++e) p = src[e] - l[e - 1] * p;
+                st = p;
+            }
+        }
+    }
     // rolled (the loop kernel runs at a 64-register cap); lanes past the end
     // (cnt < S) only repeat their last valid element
     const int e0 = BWD ? n - 1 - min(r0, n - 1) : min(r0, n - 1);
@@ -565,17 +588,21 @@ __device__ __forceinline__ bool pcg_seg_sweep(const double* __restrict__ src,
     return false;
 }
 
+#ifndef EPC_PCG_SEG_WARM
+#define EPC_PCG_SEG_WARM 1
+#endif
 template <int S, int CPW, class SIDX>
 __device__ __forceinline__ void sweeps_seg(const PcgUpdArgs& A, int nc, double* X, const double* Y,
                                            size_t base, const SIDX& sidx, int ne, int ne2) {
     const int tid = threadIdx.x, lane = tid & 31, n1 = A.n1, RS = A.tile_rs;
+    constexpr int SEG_WARM = EPC_PCG_SEG_WARM ? (S <= 9 ? 3 * S : 2 * S) : 0;  // see pcg_seg_sweep
     double* const T = const_cast<double*>(Y) + CPW * RS;  // third staged array
     const double* __restrict__ FD = A.fd;
     for (int cc = tid >> 5; cc < nc; cc += (int)(blockDim.x >> 5)) {
         const double* x = X + cc * RS;
         double* t = T + cc * RS;
         const double* y = Y + cc * RS;
-        if (!pcg_seg_sweep<S, false, false>(x, t, y, n1) && lane == 0) {
+        if (!pcg_seg_sweep<S, false, false, SEG_WARM>(x, t, y, n1) && lane == 0) {
             double prev = x[0];
             t[0] = prev;
             for (int i = 1; i < n1; ++i) {
@@ -601,7 +628,7 @@ __device__ __forceinline__ void sweeps_seg(const PcgUpdArgs& A, int nc, double* 
         double* x = X + cc * RS;
         const double* t = T + cc * RS;
         const double* y = Y + cc * RS;
-        if (!pcg_seg_sweep<S, true, false>(t, x, y, n1) && lane == 0) {
+        if (!pcg_seg_sweep<S, true, false, SEG_WARM>(t, x, y, n1) && lane == 0) {
             double nxt = t[n1 - 1];
             x[n1 - 1] = nxt;
             for (int i = n1 - 2; i >= 0; --i) {
@@ -952,11 +979,16 @@ __device__ __forceinline__ void ws_final(const PcgUpdArgs& A, size_t base, int n
 #ifndef EPC_PCG_WS_PIPE
 #define EPC_PCG_WS_PIPE 1
 #endif
+#ifndef EPC_PCG_WS_WARM
+#define EPC_PCG_WS_WARM 1
+#endif
 template <int SEG>
 __device__ __forceinline__ void ws_sweep_column(double* x, double* t, const double* y,
                                                 const double* __restrict__ fd, int n1) {
     const int lane = threadIdx.x & 31;
     constexpr bool WS_PIPE = EPC_PCG_WS_PIPE;
+    // warm-up length: about 27 steps cover the start's decay at C3 (|l| ~ 0.17)
+    constexpr int WS_WARM = EPC_PCG_WS_WARM ? (SEG <= 9 ? 3 * SEG : 2 * SEG) : 0;
     if constexpr (SEG == 0) {
         ldlt_solve_warp(x, y, fd, n1);
         (void)t;
@@ -969,7 +1001,7 @@ __device__ __forceinline__ void ws_sweep_column(double* x, double* t, const doub
 #pragma unroll
         for (int j = 0; j < SEG; ++j) dv[j] = __ldg(fd + min(r0 + j, n1 - 1));
         const double d0 = __ldg(fd);
-        if (!pcg_seg_sweep<SEG, false, WS_PIPE>(x, t, y, n1) && lane == 0) {
+        if (!pcg_seg_sweep<SEG, false, WS_PIPE, WS_WARM>(x, t, y, n1) && lane == 0) {
             double prev = x[0];
             t[0] = prev;
             for (int i = 1; i < n1; ++i) {
@@ -983,7 +1015,7 @@ __device__ __forceinline__ void ws_sweep_column(double* x, double* t, const doub
             if (j < cnt) t[r0 + j] = t[r0 + j] / dv[j];
         if (lane == 0) t[0] = t[0] / d0;
         __syncwarp();
-        if (!pcg_seg_sweep<SEG, true, WS_PIPE>(t, x, y, n1) && lane == 0) {
+        if (!pcg_seg_sweep<SEG, true, WS_PIPE, WS_WARM>(t, x, y, n1) && lane == 0) {
             double nxt = t[n1 - 1];
             x[n1 - 1] = nxt;
             for (int i = n1 - 2; i >= 0; --i) {
