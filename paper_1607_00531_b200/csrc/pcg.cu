@@ -11,9 +11,10 @@
 // and k_pcg_update_bj / k_pcg_update (d += alpha p; r += (-alpha) q;
 // z = M^{-1} r; r.r, r.z; relres, relres_prec, stop test, beta = rz_new /
 // rz). Element-wise work is bitwise the reference's. The block-Jacobi sweeps
-// run one lane per column over shared-memory tiles (k_pcg_update_bj);
-// k_pcg_update (one warp per column, lane-0 sweeps) serves the start phase
-// of the other preconditioners and the Jacobi / identity applies.
+// run over shared-memory tiles: k_pcg_update_ws (8-column groups: memory
+// warps and sweep warps pipelined over two stages) or k_pcg_update_bj
+// (one role per block; 16-column groups); k_pcg_update (one warp per
+// column, lane-0 sweeps) serves the other preconditioners.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -417,7 +418,7 @@ __device__ __forceinline__ double hvp_sweep(const PcgHvArgs& A, double beta) {
 }
 
 #ifndef EPC_HVP_MINB
-#define EPC_HVP_MINB 1
+#define EPC_HVP_MINB 4  // 64 registers, 4 blocks per SM: C3 72 -> 68 us (1, 5, 6, 8 measured)
 #endif
 __global__ void __launch_bounds__(256, EPC_HVP_MINB) k_pcg_hvp(PcgHvArgs A, PcgState* S) {
     __shared__ double sh[8];
@@ -721,18 +722,6 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
         }
     } else for (int h0 = tid; h0 < ne2; h0 += 2 * (int)blockDim.x) {
         double2 r[2], pp[2], qq[2], dd[2], l[2];
-#if EPC_PCG_EXP == 2  // timing experiment: no global traffic
-        if (true) {
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int h = h0 + u * (int)blockDim.x;
-                if (h >= ne2) break;
-                stage1(2 * h, 1.0 + a * h, 0.25);
-                stage1(2 * h + 1, 1.0 - a * h, 0.25);
-            }
-            continue;
-        }
-#endif
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int h = min(h0 + u * (int)blockDim.x, ne2 - 1);
@@ -774,13 +763,8 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
         stage1(ne - 1, r, __ldg(FL + o));
     }
     __syncthreads();
-#if EPC_PCG_EXP == 1  // timing experiment: no sweeps
-    if (COH)
-#endif
-    {
     if constexpr (SEG != 0) sweeps_seg<SEG, CPW>(A, nc, X, Y, base, sidx, ne, ne2);
     else sweeps_thread(A, nc, X, Y, base, sidx, ne, ne2);
-    }
     if constexpr (COH) {
 #pragma unroll 2
         for (int h = tid; h < ne2; h += (int)blockDim.x) {
@@ -793,16 +777,6 @@ __device__ __forceinline__ void bj_group(const PcgUpdArgs& A, double a, long lon
         }
     } else for (int h0 = tid; h0 < ne2; h0 += 2 * (int)blockDim.x) {  // loads of both pairs first
         double2 r[2];
-#if EPC_PCG_EXP == 2
-        if (true) {
-            for (int u = 0; u < 2; ++u) {
-                const int h = h0 + u * (int)blockDim.x;
-                if (h >= ne2) break;
-                rz += X[sidx(2 * h)] + X[sidx(2 * h + 1)];
-            }
-            continue;
-        }
-#endif
 #pragma unroll
         for (int u = 0; u < 2; ++u)
             r[u] = *reinterpret_cast<const double2*>(Rv + base + 2 * (size_t)min(h0 + u * (int)blockDim.x, ne2 - 1));
