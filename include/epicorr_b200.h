@@ -159,7 +159,12 @@ enum {
      * (k_seq_sums) instead of certifying it from the tree sums (diagnostic;
      * identical decisions, and the rows' residuals become bitwise the
      * reference's) */
-    EPC_MODE_EXACT_SUMS = 1 << 14
+    EPC_MODE_EXACT_SUMS = 1 << 14,
+    /* take the ADMM stop / rho decisions on the device (k_admm_decide) and
+     * keep one iteration in flight instead of reading every iteration's sums
+     * back before enqueueing the next (identical results; measured no faster
+     * at C1-C3, where the round trip is < 0.3% of an iteration) */
+    EPC_MODE_DEVICE_LOOP = 1 << 15
 };
 int epc_set_mode(epc_context* ctx, int mode_bits);
 /* Cumulative ADMM counters of the context (epc_admm_solve / _batch):

@@ -16,11 +16,18 @@
 // reference's rounded value. A comparison whose enclosures do not overlap
 // is decided; otherwise the caller computes the five sequential sums
 // exactly (k_seq_sums) and decides on those. Shared by the single-GPU loop
-// (api.cu) and the C++ slab loop (slab_nccl.cu).
+// (api.cu: on the host, or on the device in k_admm_decide) and the C++ slab
+// loop (multi_gpu_host.inc). The same IEEE operations on host and device.
 #pragma once
 
 #include <cmath>
 #include <limits>
+
+#ifdef __CUDACC__
+#define EPC_HD __host__ __device__
+#else
+#define EPC_HD
+#endif
 
 namespace epc_decide {
 
@@ -30,7 +37,7 @@ struct Iv {
 
 // Enclosure of the reference's sequential sum of n >= 1 non-negative terms
 // from any-order sum t of the same terms. Returns false when t is not finite.
-inline bool enclose_seq(double t, long long n, Iv* out) {
+EPC_HD inline bool enclose_seq(double t, long long n, Iv* out) {
     if (!std::isfinite(t)) return false;
     if (t == 0.0) {  // non-negative terms: zero only if every term is zero
         *out = {0.0, 0.0};
@@ -42,7 +49,7 @@ inline bool enclose_seq(double t, long long n, Iv* out) {
     const double g = nu / (1.0 - nu);
     const double k = 2.02 * g + 8.0 * u;
     out->lo = std::nextafter(t * (1.0 - k), 0.0);
-    out->hi = std::nextafter(t * (1.0 + k), std::numeric_limits<double>::infinity());
+    out->hi = std::nextafter(t * (1.0 + k), HUGE_VAL);
     return true;
 }
 
@@ -51,7 +58,7 @@ inline bool enclose_seq(double t, long long n, Iv* out) {
 struct Res {
     double pr, du, eps_pri, eps_dual;
 };
-inline Res residuals(const double s[5], double rho, double V, double sqrt_n, double eps_abs,
+EPC_HD inline Res residuals(const double s[5], double rho, double V, double sqrt_n, double eps_abs,
                      double eps_rel) {
     Res r;
     r.pr = std::sqrt(s[0]);
@@ -65,12 +72,12 @@ inline Res residuals(const double s[5], double rho, double V, double sqrt_n, dou
 enum { NO = 0, YES = 1, UNKNOWN = 2 };
 
 // Three-valued a <= b and a > b from enclosures.
-inline int le(double a_lo, double a_hi, double b_lo, double b_hi) {
+EPC_HD inline int le(double a_lo, double a_hi, double b_lo, double b_hi) {
     if (a_hi <= b_lo) return YES;
     if (a_lo > b_hi) return NO;
     return UNKNOWN;
 }
-inline int gt(double a_lo, double a_hi, double b_lo, double b_hi) {
+EPC_HD inline int gt(double a_lo, double a_hi, double b_lo, double b_hi) {
     const int r = le(a_lo, a_hi, b_lo, b_hi);
     return r == UNKNOWN ? UNKNOWN : 1 - r;
 }
@@ -82,7 +89,7 @@ struct Decision {
 };
 
 // Certified decisions from the device's five tree sums.
-inline Decision certified(const double tree[5], long long n, double rho, double V, double sqrt_n,
+EPC_HD inline Decision certified(const double tree[5], long long n, double rho, double V, double sqrt_n,
                           double eps_abs, double eps_rel, double mu, bool adaptive) {
     Decision d{false, false, 0};
     double lo[5], hi[5];
@@ -121,7 +128,7 @@ inline Decision certified(const double tree[5], long long n, double rho, double 
 }
 
 // The reference's decisions on exact sequential sums (the fallback).
-inline Decision exact(const double seq[5], double rho, double V, double sqrt_n, double eps_abs,
+EPC_HD inline Decision exact(const double seq[5], double rho, double V, double sqrt_n, double eps_abs,
                       double eps_rel, double mu, bool adaptive) {
     const Res r = residuals(seq, rho, V, sqrt_n, eps_abs, eps_rel);
     Decision d{true, false, 0};

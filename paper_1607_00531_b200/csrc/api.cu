@@ -103,7 +103,7 @@ enum Slot {
     S_ML0, S_ML1, S_MLI, S_MLD, S_MLB, S_MLO, S_MLIP, S_MLIM, S_MLFIP, S_MLFIM,
     S_F32_IP, S_F32_IM, S_F32_B0, S_F32_B1, S_F32_Z0, S_F32_Z1, S_F32_U0, S_F32_U1, S_F32_T0,
     S_F32_T1, S_F32_MATS, S_F32_Q, S_F32_S, S_F32_COL, S_F32_SCAL, S_F32_PART,
-    S_CTIME, S_SEQ,
+    S_CTIME, S_SEQ, S_ACTL,
     S_SN0, S_SN1, S_SN2, S_SN3, S_SN4, S_SN5, S_SN6, S_SN7, S_SN8, S_SN9, S_SNH, S_SNG,
     S_COUNT
 };
@@ -617,13 +617,157 @@ double rho_schedule(int schedule, double rho, double rho_min, double pr, double 
 
 // rho_schedule's arithmetic (admm.cpp:478-486) for an already-taken decision
 // (move: +1 primal > mu dual, -1 dual > mu primal, 0 neither)
-double rho_apply(int schedule, double rho, double rho_min, int move, double ti, double td) {
+__host__ __device__ double rho_apply(int schedule, double rho, double rho_min, int move, double ti,
+                                     double td) {
     if (schedule == EPC_RHO_FIXED) return rho;
     double next = rho;
     if (move > 0) next = rho * ti;
     else if (move < 0) next = rho / td;
-    if (schedule == EPC_RHO_ADAPTIVE_BOUNDED) next = std::max(next, rho_min);
+    if (schedule == EPC_RHO_ADAPTIVE_BOUNDED) next = (next < rho_min) ? rho_min : next;  // std::max
     return next;
+}
+
+// ---------------------------------------------------------------------------
+// The ADMM loop's per-iteration scalar work on the device (the pipelined
+// loop): the row, the certified stop / rho decisions, the rho update and the
+// error stop, taken by one thread per pair from the iteration's reduced sums
+// with the host code's operations (admm_decide.h, rho_apply), so the host
+// never has to answer before the next iteration is enqueued.
+// ---------------------------------------------------------------------------
+struct IterRec {  // one pair's outcome of one iteration, read back by the host
+    double rho_used, kkt, pr, du, eps_pri, eps_dual, lag;
+    long long err_col, sqp, qp;
+    int err_code, has_row, stop, exact;  // stop: EPC_STOP_* of a pair that stopped here, else -1
+};
+
+struct DecideArgs {
+    const double* scal_d;     // k_reduce_columns / reduce_dual / reduce_zdiff outputs
+    const long long* scal_i;
+    double *rho, *fac;        // per pair (S_PAIR)
+    int* act;
+    int *need, *restore, *was_act;  // per pair (S_ACTL)
+    double* seq_io;           // 8 per pair
+    IterRec* rec;
+    int npairs, schedule, exact_mode, dim;
+    long long nface;
+    double V, sqrt_n, eps_abs, eps_rel, mu, rho_min, tau_incr, tau_decr, alpha;
+};
+
+__device__ void decide_apply(const DecideArgs& D, int q, const epc_decide::Decision& dec) {
+    IterRec& r = D.rec[q];
+    if (dec.converged) {
+        r.stop = EPC_STOP_CONVERGED;
+        D.act[q] = 0;
+        return;
+    }
+    const double rho = D.rho[q];
+    const double next = rho_apply(D.schedule, rho, D.rho_min, dec.rho_move, D.tau_incr, D.tau_decr);
+    if (next != rho) {
+        D.fac[q] = rho / next;
+        D.rho[q] = next;
+    }
+}
+
+// phase 0: the row and the certified decision (else need[q] = 1 for the
+// sequential sums); phase 1: the decisions on those sums (admm.cpp:542-552)
+template <int PHASE>
+__global__ void k_admm_decide(DecideArgs D) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= D.npairs) return;
+    IterRec& r = D.rec[q];
+    if (PHASE == 0) {
+        r = IterRec{};
+        r.err_col = -1;
+        r.stop = -1;  // no stop this iteration (EPC_STOP_CONVERGED is 0)
+        D.fac[q] = 1.0;
+        D.restore[q] = 0;
+        D.need[q] = 0;
+        D.was_act[q] = D.act[q];
+        if (!D.act[q]) return;
+        const double* cd = D.scal_d + (size_t)q * 4;
+        const long long* ci = D.scal_i + (size_t)q * 6;
+        const double* du = D.scal_d + (size_t)D.npairs * 4 + (size_t)q * 6;
+        const double* zd = D.scal_d + (size_t)D.npairs * 10 + (size_t)q * 2;
+        if (ci[0] >= 0) {  // a column failed: stop = error, state restored
+            r.err_col = ci[0];
+            r.err_code = (int)ci[1];
+            r.stop = EPC_STOP_ERROR;
+            D.act[q] = 0;
+            D.restore[q] = 1;
+            return;
+        }
+        r.sqp = ci[2];
+        r.qp = ci[3];
+        r.has_row = 1;
+        const double rho = D.rho[q];
+        r.rho_used = rho;
+        r.kkt = cd[0];
+        const epc_decide::Res tr = epc_decide::residuals(du, rho, D.V, D.sqrt_n, D.eps_abs, D.eps_rel);
+        r.pr = tr.pr;
+        r.du = tr.du;
+        r.eps_pri = tr.eps_pri;
+        r.eps_dual = tr.eps_dual;
+        const double fval = 0.5 * D.V * cd[1] + 0.5 * D.alpha * D.V * cd[2];
+        double gs = zd[0];
+        if (D.dim == 3) gs += zd[1];
+        const double gval = 0.5 * D.alpha * D.V * gs;
+        r.lag = fval + gval + rho * D.V * du[5] + 0.5 * rho * D.V * du[0];
+        epc_decide::Decision dec{false, false, 0};
+        if (!D.exact_mode)
+            dec = epc_decide::certified(du, D.nface, rho, D.V, D.sqrt_n, D.eps_abs, D.eps_rel, D.mu,
+                                        D.schedule != EPC_RHO_FIXED);
+        if (dec.decided) {
+            decide_apply(D, q, dec);
+        } else {
+            D.need[q] = 1;
+            for (int k = 0; k < 8; ++k) D.seq_io[(size_t)q * 8 + k] = 0.0;
+        }
+    } else {
+        if (!D.need[q]) return;
+        const double* seq = D.seq_io + (size_t)q * 8;
+        const double rho = D.rho[q];
+        const epc_decide::Res ex = epc_decide::residuals(seq, rho, D.V, D.sqrt_n, D.eps_abs, D.eps_rel);
+        r.pr = ex.pr;  // bitwise the reference's row values
+        r.du = ex.du;
+        r.eps_pri = ex.eps_pri;
+        r.eps_dual = ex.eps_dual;
+        r.exact = 1;
+        decide_apply(D, q, epc_decide::exact(seq, rho, D.V, D.sqrt_n, D.eps_abs, D.eps_rel, D.mu,
+                                             D.schedule != EPC_RHO_FIXED));
+    }
+}
+
+// The iteration's state tail, per pair (one pass, nothing when no pair
+// needs it): pairs inactive at the start of the iteration carry b (the
+// b-step skipped them); a pair whose b-step failed keeps the state from
+// before the iteration (admm.cpp:553-557); a pair whose rho changed scales
+// u by rho / rho' (admm.cpp:549-552). pre = the state before the iteration,
+// nxt = the iteration's output (after the host's buffer swap, the current).
+__global__ void k_admm_tail(const double* b_pre, double* b_nxt, const double* z_pre, double* z_nxt,
+                            const double* u_pre, double* u_nxt, long long nface, int npairs,
+                            const int* was_act, const int* restore, const double* fac) {
+    __shared__ int any;
+    if (threadIdx.x == 0) {
+        int a = 0;
+        for (int q = 0; q < npairs; ++q) a |= !was_act[q] | restore[q] | (fac[q] != 1.0);
+        any = a;
+    }
+    __syncthreads();
+    if (!any) return;
+    const long long n = nface * npairs;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int q = (int)(i / nface);
+        if (restore[q]) {
+            b_nxt[i] = b_pre[i];
+            z_nxt[i] = z_pre[i];
+            u_nxt[i] = u_pre[i];
+            continue;
+        }
+        if (!was_act[q]) b_nxt[i] = b_pre[i];
+        const double a = fac[q];
+        if (a != 1.0) u_nxt[i] *= a;
+    }
 }
 
 // The reference's five sequential sums (admm_decide.h fallback), read back.
@@ -696,9 +840,11 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
         std::vector<double> rho(npairs), fac(npairs, 1.0);
         std::vector<int> active(npairs, 1), restore(npairs, 0);
         for (int q = 0; q < npairs; ++q) rho[q] = rho_io[q] > 0.0 ? rho_io[q] : cfg->rho0;
-        // host staging block: rho, factor, active
+        // host staging block: scalars, then rho, factor, active, then two
+        // slots of per-pair iteration records (the pipelined loop)
         const size_t scal_bytes = (size_t)npairs * (18 * 8 + 8) + 64;
-        char* hp = static_cast<char*>(pinned(ctx, scal_bytes + (size_t)npairs * 32));
+        const size_t rec_bytes = (size_t)npairs * sizeof(IterRec);
+        char* hp = static_cast<char*>(pinned(ctx, scal_bytes + (size_t)npairs * 32 + 2 * rec_bytes));
         auto push_pairs = [&]() {
             double* hr = reinterpret_cast<double*>(hp + scal_bytes);
             std::memcpy(hr, rho.data(), npairs * sizeof(double));
@@ -715,8 +861,159 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
         const double sqrt_n = std::sqrt((double)g.nface);
         int n_active = npairs;
         const bool batch = npairs > 1;
+        const bool adaptive = cfg->schedule != EPC_RHO_FIXED;
 
-        for (int it = 1; it <= cfg->max_iter && n_active > 0; ++it) {
+        // ---- pipelined loop (EPC_MODE_DEVICE_LOOP): decisions on the device --
+        // Iteration it+1 is enqueued before the host reads iteration it's
+        // records, so the GPU never waits on the host. Every kernel of an
+        // iteration honours the per-pair active flags (a pair that stopped
+        // carries its state), so the one iteration enqueued past a stop
+        // changes nothing. Same kernels, same operations: bitwise the
+        // synchronous loop below, rows included. Measured equal to it at
+        // C1 / C2 and 0.3% slower at C3 (scripts/probe_loop.py): the host
+        // round trip costs about what the three extra launches do, so the
+        // synchronous loop stays the default.
+        const bool device_loop = (ctx->mode & EPC_MODE_DEVICE_LOOP) != 0;
+        if (device_loop) {
+            char* actl = static_cast<char*>(slot(ctx, S_ACTL, (size_t)npairs * (16 + 64) + rec_bytes));
+            int* need_dev = reinterpret_cast<int*>(actl);
+            int* rest_dev = need_dev + npairs;
+            int* was_dev = rest_dev + npairs;
+            double* seq_io = reinterpret_cast<double*>(actl + (size_t)npairs * 16);
+            IterRec* rec_dev = reinterpret_cast<IterRec*>(seq_io + (size_t)npairs * 8);
+            IterRec* rec_h[2] = {reinterpret_cast<IterRec*>(hp + scal_bytes + (size_t)npairs * 32),
+                                 reinterpret_cast<IterRec*>(hp + scal_bytes + (size_t)npairs * 32 + rec_bytes)};
+            cudaEvent_t ev_b0[2] = {eb0, epc_event_get(ctx)}, ev_b1[2] = {eb1, epc_event_get(ctx)};
+            cudaEvent_t ev_r[2] = {epc_event_get(ctx), epc_event_get(ctx)};
+            DecideArgs D{};
+            D.scal_d = scal_d;
+            D.scal_i = scal_i;
+            D.rho = rho_dev;
+            D.fac = fac_dev;
+            D.act = act_dev;
+            D.need = need_dev;
+            D.restore = rest_dev;
+            D.was_act = was_dev;
+            D.seq_io = seq_io;
+            D.rec = rec_dev;
+            D.npairs = npairs;
+            D.schedule = cfg->schedule;
+            D.exact_mode = (ctx->mode & EPC_MODE_EXACT_SUMS) ? 1 : 0;
+            D.dim = g.dim;
+            D.nface = g.nface;
+            D.V = V;
+            D.sqrt_n = sqrt_n;
+            D.eps_abs = cfg->eps_abs;
+            D.eps_rel = cfg->eps_rel;
+            D.mu = cfg->mu;
+            D.rho_min = cfg->rho_min;
+            D.tau_incr = cfg->tau_incr;
+            D.tau_decr = cfg->tau_decr;
+            D.alpha = p->alpha;
+            const int dblk = (npairs + 31) / 32;
+            const unsigned gsm = (unsigned)std::min<long long>((long long)ctx->num_sms * 2, (nf + 255) / 256);
+            auto enqueue = [&](int k) {
+                CK(cudaEventRecord(ev_b0[k], ctx->stream));
+                BStepRun br = run_bstep(ctx, g, npairs, ip, im, B[0], Z[0], U[0], B[1], rho_dev,
+                                        act_dev, p->alpha, cfg);
+                CK(cudaEventRecord(ev_b1[k], ctx->stream));
+                const long long total = g.ncol * npairs;
+                EPC_LAUNCH(ctx, "reduce_columns", k_reduce_columns, npairs, 1024, 0, br.col_i,
+                           br.col_i + total, br.col_i + 2 * total, br.col_i + 3 * total, br.col_d,
+                           br.col_d + total, br.col_d + 2 * total, g.ncol, act_dev, scal_d, scal_i);
+                ZArgs za{};
+                za.b = B[1];
+                za.u = U[0];
+                za.z_old = Z[0];
+                za.z_new = Z[1];
+                za.u_new = U[1];
+                za.rho = rho_dev;
+                za.active = act_dev;
+                za.alpha = p->alpha;
+                run_zstep(ctx, g, npairs, M, za);
+                const int nbz = (int)std::min<long long>(g.ncol, (long long)ctx->num_sms * 4);
+                double* zp = slot_t<double>(ctx, S_PART2, (size_t)npairs * nbz * 2);
+                EPC_LAUNCH(ctx, "zdiff_sums", k_zdiff_sums, dim3(nbz, npairs), 256, 0, Z[1], g.nface,
+                           g.n1, g.m2, g.m3, 1.0 / g.h2, 1.0 / g.h3, zp);
+                double* sd2 = scal_d + (size_t)npairs * 4;
+                EPC_LAUNCH(ctx, "reduce_dual", k_reduce_partials, npairs, 256, 0, za.partials, za.nblk,
+                           6, 6, sd2);
+                EPC_LAUNCH(ctx, "reduce_zdiff", k_reduce_partials, npairs, 256, 0, zp, nbz, 2, 2,
+                           sd2 + (size_t)npairs * 6);
+                EPC_LAUNCH(ctx, "admm_decide", k_admm_decide<0>, dblk, 32, 0, D);
+                run_seq_sums_pairs(ctx, B[1], Z[1], Z[0], U[1], g.nface, npairs, seq_io, need_dev);
+                EPC_LAUNCH(ctx, "admm_decide", k_admm_decide<1>, dblk, 32, 0, D);
+                EPC_LAUNCH(ctx, "admm_tail", k_admm_tail, gsm, 256, 0, B[0], B[1], Z[0], Z[1], U[0], U[1],
+                           g.nface, npairs, was_dev, rest_dev, fac_dev);
+                std::swap(B[0], B[1]);
+                std::swap(Z[0], Z[1]);
+                std::swap(U[0], U[1]);
+                check_launch();
+                d2h(ctx, rec_h[k], rec_dev, rec_bytes);
+                CK(cudaEventRecord(ev_r[k], ctx->stream));
+            };
+            std::vector<int> live(npairs, 1);
+            auto process = [&](int it, int k) {
+                CK(cudaEventSynchronize(ev_r[k]));
+                float bms = 0.f;
+                CK(cudaEventElapsedTime(&bms, ev_b0[k], ev_b1[k]));
+                const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                for (int q = 0; q < npairs; ++q) {
+                    if (!live[q]) continue;
+                    const IterRec& r = rec_h[k][q];
+                    if (r.stop == EPC_STOP_ERROR) {
+                        status[q].stop = EPC_STOP_ERROR;
+                        std::snprintf(status[q].message, sizeof status[q].message,
+                                      "b_update: column %lld: %s", r.err_col, qp_what(r.err_code));
+                        live[q] = 0;
+                        --n_active;
+                        continue;
+                    }
+                    if (!r.has_row) continue;
+                    ctx->sqp_total += r.sqp;
+                    ctx->qp_total += r.qp;
+                    if (r.exact) ctx->dec_exact++;
+                    else ctx->dec_certified++;
+                    epc_admm_row row{};
+                    row.level = level_tag;
+                    row.iter = it;
+                    row.rho = r.rho_used;
+                    row.kkt_violation = r.kkt;
+                    row.b_update_s = bms * 1e-3;
+                    row.primal_res = r.pr;
+                    row.dual_res = r.du;
+                    row.eps_pri = r.eps_pri;
+                    row.eps_dual = r.eps_dual;
+                    row.lagrangian = r.lag;
+                    row.wall_s = wall;
+                    if (status[q].nrows < max_rows) rows[(size_t)q * max_rows + status[q].nrows] = row;
+                    status[q].nrows++;
+                    if (r.stop == EPC_STOP_CONVERGED) {
+                        status[q].stop = EPC_STOP_CONVERGED;
+                        live[q] = 0;
+                        --n_active;
+                    }
+                }
+            };
+            int last = 0;  // last enqueued iteration not yet processed
+            for (int it = 1; it <= cfg->max_iter && n_active > 0; ++it) {
+                enqueue(it & 1);
+                if (last) process(last, last & 1);
+                last = it;
+            }
+            if (last && n_active > 0) process(last, last & 1);
+            // the rho each pair ended with (changed on the device)
+            double* hr = reinterpret_cast<double*>(hp + scal_bytes);
+            d2h(ctx, hr, rho_dev, (size_t)npairs * sizeof(double));
+            sync(ctx);
+            for (int q = 0; q < npairs; ++q) rho[q] = hr[q];
+            CK(cudaEventDestroy(ev_b0[1]));
+            CK(cudaEventDestroy(ev_b1[1]));
+            CK(cudaEventDestroy(ev_r[0]));
+            CK(cudaEventDestroy(ev_r[1]));
+        }
+
+        for (int it = 1; !device_loop && it <= cfg->max_iter && n_active > 0; ++it) {
             // ---- b-step ----------------------------------------------------------
             CK(cudaEventRecord(eb0, ctx->stream));
             BStepRun br = run_bstep(ctx, g, npairs, ip, im, B[0], Z[0], U[0], B[1], rho_dev,
@@ -795,7 +1092,6 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
                 row.eps_dual = tr.eps_dual;
                 // stop test and rho schedule (admm.cpp:542-548): certified against the
                 // reference's sequential sums, else decided on those sums (admm_decide.h)
-                const bool adaptive = cfg->schedule != EPC_RHO_FIXED;
                 epc_decide::Decision dec{false, false, 0};
                 if (!(ctx->mode & EPC_MODE_EXACT_SUMS))
                     dec = epc_decide::certified(du, g.nface, rho[q], V, sqrt_n, cfg->eps_abs,

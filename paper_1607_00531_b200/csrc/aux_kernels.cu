@@ -85,12 +85,23 @@ __global__ void __launch_bounds__(256) k_dual_standalone(const double* b, const 
 // across slabs in rank order). The fallback of the certified decisions
 // (admm_decide.h): warps 1.. form the terms of the next chunk in shared
 // memory (the same rounded products the reference adds) while thread 0 adds
-// the current chunk. One CTA of SEQ_THREADS threads.
+// the current chunk. One CTA of SEQ_THREADS threads per pair; with `need`,
+// CTA q sums pair q (vectors pair-major, n per pair; io + 8 q) only when
+// need[q] is set (the device-side ADMM decisions, api.cu).
 constexpr int SEQ_CHUNK = 1024;
 __global__ void __launch_bounds__(SEQ_THREADS) k_seq_sums(const double* b, const double* z,
                                                           const double* zo, const double* u,
-                                                          long long n, double* io) {
+                                                          long long n, double* io, const int* need) {
     extern __shared__ double seq_sh[];  // [2][5][SEQ_CHUNK]
+    if (need) {
+        if (!need[blockIdx.x]) return;
+        const long long o = (long long)blockIdx.x * n;
+        b += o;
+        z += o;
+        zo += o;
+        u += o;
+        io += 8 * blockIdx.x;
+    }
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
     if (threadIdx.x == 0) {
         s0 = io[0];
@@ -154,5 +165,18 @@ void run_seq_sums(epc_context* ctx, const double* b, const double* z, const doub
                              (int)seq_sums_smem());
         attr = true;
     }
-    EPC_LAUNCH(ctx, "seq_sums", k_seq_sums, 1, SEQ_THREADS, seq_sums_smem(), b, z, zo, u, n, io_dev);
+    EPC_LAUNCH(ctx, "seq_sums", k_seq_sums, 1, SEQ_THREADS, seq_sums_smem(), b, z, zo, u, n, io_dev,
+               (const int*)nullptr);
+}
+
+void run_seq_sums_pairs(epc_context* ctx, const double* b, const double* z, const double* zo,
+                        const double* u, long long n, int npairs, double* io_dev, const int* need) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_seq_sums, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)seq_sums_smem());
+        attr = true;
+    }
+    EPC_LAUNCH(ctx, "seq_sums", k_seq_sums, npairs, SEQ_THREADS, seq_sums_smem(), b, z, zo, u, n, io_dev,
+               need);
 }

@@ -112,11 +112,14 @@ __global__ void k_reduce_columns(const int* col_err, const int* col_sqp, const i
 // the reference's five sequential dual-update sums (fallback of admm_decide.h)
 constexpr int SEQ_THREADS = 512;
 __global__ void k_seq_sums(const double* b, const double* z, const double* zo, const double* u,
-                           long long n, double* io);
+                           long long n, double* io, const int* need);
 size_t seq_sums_smem();
 // launches k_seq_sums (one CTA) on the context stream; io_dev: 5 doubles in/out
 void run_seq_sums(epc_context* ctx, const double* b, const double* z, const double* zo,
                   const double* u, long long n, double* io_dev);
+// per pair q with need[q] != 0: io[8 q .. 8 q + 4] += the five sums of pair q
+void run_seq_sums_pairs(epc_context* ctx, const double* b, const double* z, const double* zo,
+                        const double* u, long long n, int npairs, double* io_dev, const int* need);
 __global__ void k_scale_pairs(double* u, long long nface, int npairs, const double* factor);
 __global__ void k_copy_masked(const double* src, double* dst, long long nface, int npairs,
                               const int* mask);

@@ -135,6 +135,7 @@ class Context:
     MODE_BSTEP_TIMING = 1
     MODE_BSTEP_CHAINED = 1 << 13
     MODE_EXACT_SUMS = 1 << 14
+    MODE_DEVICE_LOOP = 1 << 15
 
     def guard_check(self):
         """First scratch slot whose guard zones were overwritten, or -1
