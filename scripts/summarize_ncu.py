@@ -76,7 +76,8 @@ def pcg(src, dst, pcg_iters, faces):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     tot = sum(float(d[k][0].replace(",", "")) * scale[d[k][1]]
               for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-    tu = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
+    tu = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6,
+          "ms": 1e-3}
     t = float(d["gpu__time_duration.sum"][0].replace(",", "")) * tu[d["gpu__time_duration.sum"][1]]
     n, f = int(pcg_iters), int(faces)
     d["pcg_iterations"] = n
