@@ -904,18 +904,37 @@ __global__ void __launch_bounds__(F32_NT) k_dct_gemm_f32(DctGemmF32 p) {
                 for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
         }
     }
+    // index arithmetic per column in 32 bits (64-bit division is ~100
+    // instructions); lam23's index f / n1 = row (kstride / n1) + cmap / n1
+    // when the transformed axis' stride is a multiple of n1 (always here)
+    const bool narrow = p.N <= 0x7fffffffLL && (long long)p.M * p.kstride <= 0x7fffffffLL;
+    const bool ksplit = narrow && p.kstride % p.n1 == 0;
+    const unsigned kq = ksplit ? (unsigned)(p.kstride / p.n1) : 0u;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
         const long long col = col0 + tx + 16 * c;
         if (col >= p.N) continue;
-        const long long cmap = (col / p.cdiv) * p.cstride + (col % p.cdiv);
+        long long cmap;
+        unsigned cq = 0;
+        if (narrow) {
+            const unsigned cu = (unsigned)col, cd = (unsigned)p.cdiv;
+            const unsigned qd = cu / cd;
+            cmap = (long long)qd * p.cstride + (long long)(cu - qd * cd);
+            if (EPI == EPI_DIVIDE && ksplit) cq = (unsigned)cmap / (unsigned)p.n1;
+        } else {
+            cmap = (col / p.cdiv) * p.cstride + (col % p.cdiv);
+        }
 #pragma unroll
         for (int r = 0; r < RM; ++r) {
             const int row = row0 + ty + 16 * r;
             if (row >= p.M) continue;
             const long long f = (long long)row * p.kstride + cmap;
             float v = acc[r][c];
-            if (EPI == EPI_DIVIDE) v = v / (p.aV * p.lam23[f / p.n1] + p.rV);
+            if (EPI == EPI_DIVIDE) {
+                const long long li = ksplit ? (long long)((unsigned)row * kq + cq)
+                                            : (narrow ? (long long)((unsigned)f / (unsigned)p.n1) : f / p.n1);
+                v = v / (p.aV * p.lam23[li] + p.rV);
+            }
             p.out[f] = v;
         }
     }

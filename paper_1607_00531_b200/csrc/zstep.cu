@@ -124,11 +124,25 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
 
     double ps[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     const bool act = (EPI == EPI_DUAL) ? (p.active == nullptr || p.active[pair] != 0) : true;
+    // column index arithmetic once per column, in 32 bits when N allows
+    // (every configuration here; 64-bit division costs ~100 instructions)
+    const bool narrow = p.N <= 0x7fffffffLL;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         const long long col = col0 + tx + 16 * c;
         if (col >= p.N) continue;
-        const long long cmap = (col / p.cdiv) * p.cstride + (col % p.cdiv);
+        long long cmap;
+        int cq = 0;
+        if (narrow) {
+            const unsigned cu = (unsigned)col, cd = (unsigned)p.cdiv;
+            const unsigned qd = cu / cd;
+            cmap = (long long)qd * p.cstride + (long long)(cu - qd * cd);
+            if (EPI == EPI_DIVIDE) cq = (int)(cu / (unsigned)p.n1);
+        } else {
+            cmap = (col / p.cdiv) * p.cstride + (col % p.cdiv);
+            if (EPI == EPI_DIVIDE) cq = (int)(col / p.n1);
+        }
+        const int cbase = (EPI == EPI_DIVIDE) ? (p.div_axis == 3 ? cq : p.m2 * (cq % p.m3)) : 0;
 #pragma unroll
         for (int r = 0; r < RM; ++r) {
             const int row = row0 + ty + 16 * r;
@@ -136,9 +150,8 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
             const long long f = zoff + (long long)row * p.kstride + cmap;
             double v = acc[r][c];
             if (EPI == EPI_DIVIDE) {
-                int cidx;
-                if (p.div_axis == 3) cidx = (int)(col / p.n1) + p.m2 * row;
-                else cidx = row + p.m2 * (int)((col / p.n1) % p.m3);
+                // axis 3: j = col / n1, cidx = j + m2 q3; axis 2: k = (col / n1) % m3, cidx = q2 + m2 k
+                const int cidx = p.div_axis == 3 ? cbase + p.m2 * row : row + cbase;
                 const double denom = p.alpha * p.V * p.lam23[cidx] + p.rho[pair] * p.V;
                 p.out[f] = v / denom;
             } else if (EPI == EPI_DUAL) {
