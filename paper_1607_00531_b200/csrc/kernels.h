@@ -86,6 +86,7 @@ struct GemmParams {
     double* u_new;
     double* partials;  // per CTA: 6 sums
     const int* active;
+    int mfirst;  // set by the launcher: M tiles in grid x
 };
 enum { PRO_PLAIN = 0, PRO_RHS = 1 };
 enum { EPI_STORE = 0, EPI_DIVIDE = 1, EPI_DUAL = 2 };

@@ -21,10 +21,14 @@
 #include "kernels.h"
 
 #include <cstdlib>
+#include <string>
 
 namespace {
 #ifndef EPC_GEMM_BK
 #define EPC_GEMM_BK 16  // k-slab depth; 32 measured slower for three of the four transforms
+#endif
+#ifndef EPC_GEMM_MFIRST
+#define EPC_GEMM_MFIRST 1
 #endif
 constexpr int BN = 64, BK = EPC_GEMM_BK, NT = 256;
 constexpr int AR = NT / BK;  // A-tile rows loaded per pass (a thread per k column)
@@ -42,8 +46,13 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
     __shared__ double Bs[BK][BN];
     __shared__ double red[(NT / 32) * 6];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const int row0 = blockIdx.y * BM;
-    const long long col0 = (long long)blockIdx.x * BN;
+    // M tiles innermost in launch order: the CTAs sharing one B (column)
+    // tile run together and its re-reads hit L2 (EPC_GEMM_MFIRST=0: N first)
+    const bool mf = p.mfirst != 0;
+    const int tm = mf ? blockIdx.x : blockIdx.y, tn = mf ? blockIdx.y : blockIdx.x;
+    const int ntm = mf ? gridDim.x : gridDim.y, ntn = mf ? gridDim.y : gridDim.x;
+    const int row0 = tm * BM;
+    const long long col0 = (long long)tn * BN;
     const int pair = blockIdx.z;
     const long long zoff = (long long)pair * p.zstride;
 
@@ -188,28 +197,36 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
         if (tid < 6) {
             double t = 0.0;
             for (int i = 0; i < NT / 32; ++i) t += red[i * 6 + tid];
-            const long long blk = (long long)blockIdx.y * gridDim.x + blockIdx.x;
-            const long long nblk = (long long)gridDim.x * gridDim.y;
+            const long long blk = (long long)tm * ntn + tn;  // the same order either way
+            const long long nblk = (long long)ntm * ntn;
             p.partials[((long long)pair * nblk + blk) * 6 + tid] = t;
         }
     }
 }
 
+// M tiles in grid x (launched first) unless the column tiles exceed grid y
+static dim3 gemm_grid(GemmParams& p, int BM, int nz) {
+    const unsigned tn = (unsigned)((p.N + BN - 1) / BN), tm = (unsigned)((p.M + BM - 1) / BM);
+    p.mfirst = EPC_GEMM_MFIRST && tn <= 65535u;
+    return p.mfirst ? dim3(tm, tn, (unsigned)nz) : dim3(tn, tm, (unsigned)nz);
+}
+
 void launch_dct_gemm_64(epc_context* ctx, const char* name, const GemmParams& p, int pro, int epi,
                         int nz, int* nblocks_out) {
     constexpr int BM = 64;
-    dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + BM - 1) / BM), (unsigned)nz);
+    GemmParams q = p;
+    const dim3 grid = gemm_grid(q, BM, nz);
     if (nblocks_out) *nblocks_out = (int)(grid.x * grid.y);
     if (pro == PRO_RHS && epi == EPI_STORE)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_STORE, 4>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_STORE, 4>), grid, NT, 0, q);
     else if (pro == PRO_RHS && epi == EPI_DIVIDE)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_DIVIDE, 4>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_DIVIDE, 4>), grid, NT, 0, q);
     else if (pro == PRO_PLAIN && epi == EPI_DIVIDE)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DIVIDE, 4>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DIVIDE, 4>), grid, NT, 0, q);
     else if (pro == PRO_PLAIN && epi == EPI_DUAL)
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DUAL, 4>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DUAL, 4>), grid, NT, 0, q);
     else
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_STORE, 4>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_STORE, 4>), grid, NT, 0, q);
 }
 
 // 96-row tiles for the plain-store transforms when M is a multiple of 96
@@ -222,9 +239,10 @@ void launch_dct_gemm(epc_context* ctx, const char* name, const GemmParams& p, in
     static const bool force64 = getenv("EPC_GEMM_RM") && atoi(getenv("EPC_GEMM_RM")) == 4;
     if (!force64 && pro == PRO_PLAIN && epi == EPI_STORE && p.M % 96 == 0) {
         constexpr int BM = 96;
-        dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + BM - 1) / BM), (unsigned)nz);
+        GemmParams q = p;
+        const dim3 grid = gemm_grid(q, BM, nz);
         if (nblocks_out) *nblocks_out = (int)(grid.x * grid.y);
-        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_STORE, 6>), grid, NT, 0, p);
+        EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_STORE, 6>), grid, NT, 0, q);
     } else {
         launch_dct_gemm_64(ctx, name, p, pro, epi, nz, nblocks_out);
     }
