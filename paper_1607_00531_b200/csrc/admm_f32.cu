@@ -518,11 +518,11 @@ __global__ void __launch_bounds__(32, 16) k_bstep_f32(BStepF32Params P) {
             // model at x: r, jlo, jhi per cell; fval pieces
             double sr = 0.0, sd = 0.0, sq = 0.0;
             for (int c = lane; c < m1; c += 32) {
-                const float a = 0.5f * (x[c] + x[c + 1]), d = (x[c + 1] - x[c]) / h, t = a * ih;
+                const float a = 0.5f * (x[c] + x[c + 1]), d = (x[c + 1] - x[c]) * ih, t = a * ih;
                 const float vp = ipv_l(ip, m1, c, t), vm = ipv_l(im, m1, c, -t);
                 const float gp = ips_l(ip, m1, ih, c, t), gm = ips_l(im, m1, ih, c, -t);
                 const float r = vp * (1.0f + d) - vm * (1.0f - d);
-                const float wa = 0.5f * (gp * (1.0f + d) + gm * (1.0f - d)), wd = (vp + vm) / h;
+                const float wa = 0.5f * (gp * (1.0f + d) + gm * (1.0f - d)), wd = (vp + vm) * ih;
                 R[c] = r;
                 JL[c] = wa - wd;
                 JH[c] = wa + wd;
@@ -535,12 +535,12 @@ __global__ void __launch_bounds__(32, 16) k_bstep_f32(BStepF32Params P) {
                 sq += (double)e * e;
                 float g = rw * e, dg = rw, og = 0.0f;
                 if (i < m1) {
-                    g += V * JL[i] * R[i] - aw * ((x[i + 1] - x[i]) / h) / h;
+                    g += V * JL[i] * R[i] - aw * ((x[i + 1] - x[i]) * ih) * ih;
                     dg += V * JL[i] * JL[i] + lapw;
                     og = V * JL[i] * JH[i] - lapw;
                 }
                 if (i > 0) {
-                    g += V * JH[i - 1] * R[i - 1] + aw * ((x[i] - x[i - 1]) / h) / h;
+                    g += V * JH[i - 1] * R[i - 1] + aw * ((x[i] - x[i - 1]) * ih) * ih;
                     dg += V * JH[i - 1] * JH[i - 1] + lapw;
                 }
                 grad[i] = g;
@@ -573,10 +573,12 @@ __global__ void __launch_bounds__(32, 16) k_bstep_f32(BStepF32Params P) {
             float xs = 0.0f;  // fp32: relative to |x| only (see qp_f32)
             for (int i = lane; i < n1; i += 32) {
                 const float d = qx[i] - x[i];
+                cq[i] = d;  // the search direction for the trials (cq is free after the QP)
                 sn += (double)d * d;
                 gdir += (double)grad[i] * d;
                 xs = fmaxf(xs, fabsf(x[i]));
             }
+            __syncwarp();
             sn = sqrt(wsumd(sn));
             gdir = wsumd(gdir);
             xs = wmaxf(xs);
@@ -590,13 +592,13 @@ __global__ void __launch_bounds__(32, 16) k_bstep_f32(BStepF32Params P) {
                 ++nls;
                 double tr = 0.0, td = 0.0, tq = 0.0;
                 for (int f = lane; f < n1; f += 32) {
-                    const float xf = x[f] + tls * (qx[f] - x[f]);
+                    const float xf = x[f] + tls * cq[f];
                     const float e = xf - tg[f];
                     tq += (double)e * e;
                     if (f < m1) {
-                        const float xb = x[f + 1] + tls * (qx[f + 1] - x[f + 1]);
+                        const float xb = x[f + 1] + tls * cq[f + 1];
                         const float r = cell_r(P, ip, im, f, xf, xb);
-                        const float d = (xb - xf) / h;
+                        const float d = (xb - xf) * ih;
                         tr += (double)r * r;
                         td += (double)d * d;
                     }
@@ -612,7 +614,7 @@ __global__ void __launch_bounds__(32, 16) k_bstep_f32(BStepF32Params P) {
                 tls *= 0.5f;
             }
             if (!acc) break;
-            for (int i = lane; i < n1; i += 32) x[i] = x[i] + tls * (qx[i] - x[i]);
+            for (int i = lane; i < n1; i += 32) x[i] = x[i] + tls * cq[i];
             __syncwarp();
         }
         if (err) {
