@@ -61,6 +61,10 @@ __device__ __forceinline__ float wminf(float v) {
 // displacement a, so the position is carried as u = c + t, t = +-a/h, split
 // into the integer cell i and the fraction w; the reference's edge cases are
 // the same tests written on (i, w).
+#ifndef EPC_F32_BRANCHY
+#define EPC_F32_BRANCHY 0
+#endif
+#if EPC_F32_BRANCHY
 __device__ __forceinline__ float ipv_l(const float* s, int m, int c, float t) {
     const float ft = floorf(t);
     const int i = c + (int)ft;
@@ -81,6 +85,40 @@ __device__ __forceinline__ float ips_l(const float* s, int m, float ih, int c, f
     if (i < 0) return 2.0f * s[0] * ih;
     return (s[i + 1] - s[i]) * ih;
 }
+#else
+// Branch-free forms of the two above (the same cases in the same order, every
+// case's value formed and the tests selecting one; loads clamped in range)
+__device__ __forceinline__ float ipv_l(const float* s, int m, int c, float t) {
+    const float ft = floorf(t);
+    const int i = c + (int)ft;
+    const float w = t - ft;  // u = i + w, 0 <= w < 1
+    const int ic = min(max(i, 0), max(m - 2, 0));
+    const float v_in = (1.0f - w) * s[ic] + w * s[ic + 1];
+    const float v_lo = ((float)(i + 1) + (w - 0.5f)) * 2.0f * s[0];
+    const float v_hi = ((float)(m - 1 - i) + (0.5f - w)) * 2.0f * s[m - 1];
+    const bool zero = i < -1 || (i == -1 && w <= 0.5f) || i > m - 1 || (i == m - 1 && w >= 0.5f);
+    const bool lo = i < 0 || (i == 0 && w == 0.0f);
+    float v = (i >= m - 1) ? v_hi : v_in;
+    v = lo ? v_lo : v;
+    return zero ? 0.0f : v;
+}
+__device__ __forceinline__ float ips_l(const float* s, int m, float ih, int c, float t) {
+    const float ft = floorf(t);
+    const int i0 = c + (int)ft;
+    const float w = t - ft;
+    const float n_lo = 2.0f * s[0] * ih, n_hi = -2.0f * s[m - 1] * ih;
+    const int i = (w == 0.0f) ? i0 - 1 : i0;  // fi == u: the left interval
+    const int ic = min(max(i, 0), max(m - 2, 0));
+    const float v_in = (s[ic + 1] - s[ic]) * ih;
+    const bool zero = i0 < -1 || (i0 == -1 && w <= 0.5f) || i0 > m - 1 || (i0 == m - 1 && w > 0.5f);
+    const bool lo = i0 < 0 || (i0 == 0 && w == 0.0f);
+    const bool hi = i0 > m - 1 || (i0 == m - 1 && w > 0.0f);
+    float v = (i < 0) ? n_lo : v_in;
+    v = hi ? n_hi : v;
+    v = lo ? n_lo : v;
+    return zero ? 0.0f : v;
+}
+#endif
 
 // residual of cell c at faces (xa, xb) (residual_column, objective.cpp:48-73)
 __device__ __forceinline__ float cell_r(const BStepF32Params& P, const float* ip, const float* im,
