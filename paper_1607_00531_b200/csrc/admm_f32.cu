@@ -803,9 +803,20 @@ __global__ void __launch_bounds__(256) k_dual_f32(const float* b, const float* z
         acc[3] += (double)zi * zi;
         acc[4] += (double)uu * uu;
         acc[5] += (double)uu * df;
-        const long long c = i / n1;
-        const int j = (int)(c % m2);
-        const long long k = c / m2;
+        // 32-bit index arithmetic when the volume allows (64-bit division
+        // costs ~100 instructions)
+        int j;
+        long long k;
+        if (n <= 0xffffffffLL) {
+            const unsigned c = (unsigned)i / (unsigned)n1;
+            const unsigned kq = c / (unsigned)m2;
+            j = (int)(c - kq * (unsigned)m2);
+            k = kq;
+        } else {
+            const long long c = i / n1;
+            j = (int)(c % m2);
+            k = c / m2;
+        }
         if (j + 1 < m2) {
             const float o = (z[i + n1] - zi) * ih2;
             acc[6] += (double)o * o;
