@@ -258,23 +258,50 @@ __global__ void __launch_bounds__(256) k_zdiff_sums(const double* z, long long n
     const int pair = blockIdx.y;
     const double* zp = z + (long long)pair * nface;
     const long long layer = (long long)n1 * m2;
-    const int ncol = m2 * m3;
     double s2 = 0.0, s3 = 0.0;
-    // block per column range, threads along the contiguous column (coalesced,
-    // no 64-bit index division per element)
-    for (int c = blockIdx.x; c < ncol; c += gridDim.x) {
-        const int j = c % m2, k = c / m2;
-        const double* zc = zp + (long long)c * n1;
-        const bool hj = j + 1 < m2, hk = m3 > 1 && k + 1 < m3;
-        for (int i = threadIdx.x; i < n1; i += blockDim.x) {
-            const double zf = zc[i];
-            if (hj) {
-                const double o = (zc[i + n1] - zf) * ih2;
-                s2 += o * o;
+    // block b owns one contiguous range of faces; each thread walks it with a
+    // stride of the block size, ZU faces' loads in flight, tracking its
+    // position in the layer incrementally (no index division per face):
+    // (D2 z) exists unless the face is in the layer's last column, (D3 z)
+    // unless it is in the last layer
+    constexpr int ZU = 4;
+    const long long per = (nface + gridDim.x - 1) / gridDim.x;
+    const long long f0 = (long long)blockIdx.x * per;
+    const long long f1 = f0 + per < nface ? f0 + per : nface;
+    long long f = f0 + threadIdx.x;
+    long long k = f / layer, off = f - k * layer;  // once per thread
+    const long long step = blockDim.x;
+    const long long jlim = layer - n1, klim = m3 - 1;
+    for (; f < f1; f += ZU * step) {
+        double zf[ZU], zj[ZU], zk[ZU];
+        bool hj[ZU], hk[ZU], in[ZU];
+        long long o = off, kk = k;
+#pragma unroll
+        for (int u = 0; u < ZU; ++u) {
+            const long long g = f + u * step;
+            in[u] = g < f1;
+            hj[u] = in[u] && o < jlim;
+            hk[u] = in[u] && kk < klim;
+            zf[u] = in[u] ? zp[g] : 0.0;
+            zj[u] = hj[u] ? zp[g + n1] : 0.0;
+            zk[u] = hk[u] ? zp[g + layer] : 0.0;
+            o += step;
+            while (o >= layer) {  // once at most unless a layer is smaller than a block
+                o -= layer;
+                ++kk;
             }
-            if (hk) {
-                const double o = (zc[i + layer] - zf) * ih3;
-                s3 += o * o;
+        }
+        off = o;
+        k = kk;
+#pragma unroll
+        for (int u = 0; u < ZU; ++u) {
+            if (hj[u]) {
+                const double d = (zj[u] - zf[u]) * ih2;
+                s2 += d * d;
+            }
+            if (hk[u]) {
+                const double d = (zk[u] - zf[u]) * ih3;
+                s3 += d * d;
             }
         }
     }
