@@ -237,7 +237,18 @@ void launch_dct_gemm_64(epc_context* ctx, const char* name, const GemmParams& p,
 void launch_dct_gemm(epc_context* ctx, const char* name, const GemmParams& p, int pro, int epi,
                      int nz, int* nblocks_out) {
     static const bool force64 = getenv("EPC_GEMM_RM") && atoi(getenv("EPC_GEMM_RM")) == 4;
-    if (!force64 && pro == PRO_PLAIN && epi == EPI_STORE && p.M % 96 == 0) {
+    if (!force64 && epi == EPI_DIVIDE && p.M % 64 != 0 && p.M % 48 == 0) {
+        // 48-row tiles: no half-empty second tile at m3 = 96, and the divide
+        // epilogue's registers stay at the 64-row kernel's occupancy
+        constexpr int BM = 48;
+        GemmParams q = p;
+        const dim3 grid = gemm_grid(q, BM, nz);
+        if (nblocks_out) *nblocks_out = (int)(grid.x * grid.y);
+        if (pro == PRO_RHS)
+            EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_RHS, EPI_DIVIDE, 3>), grid, NT, 0, q);
+        else
+            EPC_LAUNCH(ctx, name, (k_dct_gemm<PRO_PLAIN, EPI_DIVIDE, 3>), grid, NT, 0, q);
+    } else if (!force64 && pro == PRO_PLAIN && epi == EPI_STORE && p.M % 96 == 0) {
         constexpr int BM = 96;
         GemmParams q = p;
         const dim3 grid = gemm_grid(q, BM, nz);
