@@ -929,6 +929,11 @@ def main():
     # The DCT GEMMs are fp64-pipe bound: 2*M*K*N unfused mul+add per transform
     # (exact k order, no FMA), against the measured fp64 issue rate
     # (scripts/ubench_fp64_tput.cu -> profiles/r01_ubench_fp64_tput.log).
+    # the forward axis-2 transform fused into the b-step's drain (the default
+    # at C3, bstep.cu: bstep_drain_fwd2): its bytes belong to the b-step launch
+    fwd2_fused = "dct_fwd2" not in prof and g.m[2] > 1
+    if fwd2_fused:
+        alg["admm_bstep"] += alg.pop("dct_fwd2")
     m1_, m2_, m3_ = g.m
     n1_ = m1_ + 1
     pairs_ = npairs if a.config == "C4" else 1
@@ -972,7 +977,9 @@ def main():
     roofline = {"bound": "hbm", "kernel": bname, "achieved": b_ach, "peak": hbm_peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": b_ach / hbm_peak,
                 "traffic": traffic, "traffic_source": traffic_src, "share_of_step": bms / sum(v[0] for v in prof.values()),
-                "note": "b-step is fp64-latency bound (serial SQP/QP chains), not HBM bound",
+                "note": "b-step is fp64-latency bound (serial SQP/QP chains), not HBM bound"
+                        + ("; the forward axis-2 DCT runs in its drain (bytes included)" if fwd2_fused else ""),
+                "fwd2_fused": fwd2_fused,
                 "bstep_pipes": pipe,
                 "kernels": kernels}
 
@@ -997,7 +1004,11 @@ def main():
         x400 = run_x400_leg(a, ctx, dev, stream, flush, iters, rank, dist)
     sharded = None
     if a.config == "C3" and (world > 1 or a.sharded) and dist is not None:
-        sharded = run_sharded_legs(a, ctx, dev, stream, dist, rank, world)
+        try:  # the headline line must survive a failure in the sharded legs
+            sharded = run_sharded_legs(a, ctx, dev, stream, dist, rank, world)
+        except Exception as e:
+            sharded = {"error": f"{type(e).__name__}: {e}"[:300]}
+            print(f"[bench] sharded legs failed on rank {rank}: {e}", file=sys.stderr, flush=True)
     f32 = None
     if not a.no_f32 and a.config != "C4":
         f32 = run_f32_leg(a, ctx, dev, stream, flush, g, ipn, imn, iters, last_b, dist)

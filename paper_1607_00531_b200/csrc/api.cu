@@ -103,7 +103,7 @@ enum Slot {
     S_ML0, S_ML1, S_MLI, S_MLD, S_MLB, S_MLO, S_MLIP, S_MLIM, S_MLFIP, S_MLFIM,
     S_F32_IP, S_F32_IM, S_F32_B0, S_F32_B1, S_F32_Z0, S_F32_Z1, S_F32_U0, S_F32_U1, S_F32_T0,
     S_F32_T1, S_F32_MATS, S_F32_Q, S_F32_S, S_F32_COL, S_F32_SCAL, S_F32_PART,
-    S_CTIME, S_SEQ, S_ACTL,
+    S_CTIME, S_SEQ, S_ACTL, S_FUSE,
     S_SN0, S_SN1, S_SN2, S_SN3, S_SN4, S_SN5, S_SN6, S_SN7, S_SN8, S_SN9, S_SNH, S_SNG,
     S_COUNT
 };
@@ -277,6 +277,7 @@ struct ZArgs {
     double* partials;  // dual partials [npairs][nblk][6]
     int nblk;          // out: blocks per pair of the dual GEMM
     bool rhs_is_raw;   // true: b holds the rhs itself (dct_solve), u unused
+    bool fwd2_done;    // h1 already holds the forward axis-2 transform (fused in the b-step)
 };
 
 void run_zstep(epc_context* ctx, const Geo& g, int npairs, const DctMats& M, ZArgs& a) {
@@ -317,7 +318,7 @@ void run_zstep(epc_context* ctx, const Geo& g, int npairs, const DctMats& M, ZAr
         f2.in0 = a.b;
         f2.in1 = a.u;
         f2.out = h1;
-        launch_dct_gemm(ctx, "dct_fwd2", f2, pro, EPI_STORE, npairs, nullptr);
+        if (!a.fwd2_done) launch_dct_gemm(ctx, "dct_fwd2", f2, pro, EPI_STORE, npairs, nullptr);
         GemmParams f3 = p;
         axis3(f3);
         f3.A = M.c3;
@@ -368,12 +369,13 @@ void run_zstep(epc_context* ctx, const Geo& g, int npairs, const DctMats& M, ZAr
 struct BStepRun {
     int* col_i;     // err, sqp, qp, maxact (4 x total)
     double* col_d;  // kkt, fr, fd (3 x total)
+    bool fwd2_fused;  // the z-step's forward axis-2 transform ran in the b-step's drain
 };
 
 BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip, const double* im,
                    const double* b, const double* z, const double* u, double* b_out,
                    const double* rho_dev, const int* active_dev, double alpha,
-                   const epc_admm_config* cfg) {
+                   const epc_admm_config* cfg, const Fwd2Params* fwd2 = nullptr) {
     const long long total = g.ncol * npairs;
     const HDiv hd = make_hdiv(g.h1);
     // EPC_BSTEP_TAIL (dev aid): per-CTA exit times and per-column durations,
@@ -452,6 +454,17 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
     P.total_cols = total;
     P.timing = (ctx->mode & EPC_MODE_BSTEP_TIMING) ? slot_t<long long>(ctx, S_GN9, 28) : nullptr;
     P.cert = (ctx->mode & EPC_MODE_BSTEP_CHAINED) ? 0 : 1;
+    // the fused forward axis-2 transform needs 8.3 KB of the drained column's
+    // shared memory (long enough columns: n1 >= 87) and a separate axis 3
+    const bool fuse = fwd2 != nullptr && g.m3 > 1 && smem >= (size_t)(16 * 33 + 16 * 32) * 8;
+    if (fuse) {
+        P.fwd2 = *fwd2;
+        const size_t nl = (size_t)npairs * g.m3;
+        unsigned long long* fc = slot_t<unsigned long long>(ctx, S_FUSE, 1 + (nl + 1) / 2);
+        CK(cudaMemsetAsync(fc, 0, (1 + (nl + 1) / 2) * 8, ctx->stream));
+        P.fwd2.tile_counter = fc;
+        P.fwd2.layer_done = reinterpret_cast<unsigned*>(fc + 1);
+    }
     if (tail && total < (1LL << 31)) P.col_ns = slot_t<unsigned>(ctx, S_CTIME, (size_t)total);
     P.cta_span = tail ? slot_t<unsigned long long>(ctx, S_GN8, (size_t)slots * 2) : nullptr;
     static const char* dump = getenv("EPC_BSTEP_DUMP");  // dev aid: per-column records
@@ -530,7 +543,7 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
         }
     }
     check_launch();
-    return BStepRun{col_i, col_d};
+    return BStepRun{col_i, col_d, fuse};
 }
 
 // ---------------------------------------------------------------------------
@@ -1013,11 +1026,36 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
             CK(cudaEventDestroy(ev_r[1]));
         }
 
+        // the forward axis-2 transform in the b-step's drain (BStepParams::fwd2);
+        // EPC_FUSE_FWD2=0: the separate GEMM launch (dev A/B; same bits)
+        static const bool fuse_env = !getenv("EPC_FUSE_FWD2") || atoi(getenv("EPC_FUSE_FWD2")) != 0;
+        // Only after a short b-step: with a long tail (x400: 40-80 ms launches)
+        // the drain's transform is a sliver of the launch and its warps
+        // compete with the tail columns (EPC_FUSE_MAX_MS, default 12 ms)
+        static const double fuse_max_ms = getenv("EPC_FUSE_MAX_MS") ? atof(getenv("EPC_FUSE_MAX_MS")) : 12.0;
+        const bool fuse_fwd2_ok = fuse_env && g.m3 > 1;
+        double prev_bstep_ms = -1.0;  // the previous iteration's b-step (events eb0 / eb1)
         for (int it = 1; !device_loop && it <= cfg->max_iter && n_active > 0; ++it) {
             // ---- b-step ----------------------------------------------------------
             CK(cudaEventRecord(eb0, ctx->stream));
+            const bool fuse_fwd2 = fuse_fwd2_ok && prev_bstep_ms >= 0.0 && prev_bstep_ms < fuse_max_ms;
+            Fwd2Params f2{};
+            if (fuse_fwd2) {
+                f2.A = M.c2;
+                f2.b = B[1];
+                f2.u = U[0];
+                f2.rho = rho_dev;
+                f2.out = slot_t<double>(ctx, S_H1, (size_t)g.nface * npairs);
+                f2.V = g.V;
+                f2.nface = g.nface;
+                f2.n1 = g.n1;
+                f2.m2 = g.m2;
+                f2.m3 = g.m3;
+                f2.npairs = npairs;
+            }
             BStepRun br = run_bstep(ctx, g, npairs, ip, im, B[0], Z[0], U[0], B[1], rho_dev,
-                                    batch ? act_dev : nullptr, p->alpha, cfg);
+                                    batch ? act_dev : nullptr, p->alpha, cfg,
+                                    fuse_fwd2 ? &f2 : nullptr);
             CK(cudaEventRecord(eb1, ctx->stream));
             const long long total = g.ncol * npairs;
             EPC_LAUNCH(ctx, "reduce_columns", k_reduce_columns, npairs, 1024, 0, br.col_i,
@@ -1034,6 +1072,7 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
             za.rho = rho_dev;
             za.active = batch ? act_dev : nullptr;
             za.alpha = p->alpha;
+            za.fwd2_done = br.fwd2_fused;
             run_zstep(ctx, g, npairs, M, za);
             const int nbz = (int)std::min<long long>(g.ncol, (long long)ctx->num_sms * 4);
             double* zp = slot_t<double>(ctx, S_PART2, (size_t)npairs * nbz * 2);
@@ -1053,6 +1092,7 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
             sync(ctx);
             float bms = 0.f;
             CK(cudaEventElapsedTime(&bms, eb0, eb1));
+            prev_bstep_ms = bms;
             const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 
             bool any_restore = false, any_rho = false;

@@ -7,7 +7,23 @@
 #include "model.cuh"
 
 // ---- ADMM b-step (bstep.cu) ---------------------------------------------
+// The z-step's forward axis-2 transform fused into the b-step's drain
+// (bstep.cu: bstep_drain_fwd2): out = C2 x (rho V (b + u)) per k-layer, each
+// layer started once its m2 columns are counted done in layer_done.
+struct Fwd2Params {
+    const double* A;  // C2, m2 x m2 row-major
+    const double *b, *u;
+    const double* rho;
+    double* out;
+    double V;
+    long long nface;
+    int n1, m2, m3, npairs;
+    unsigned* layer_done;                // [npairs * m3], zeroed before the launch
+    unsigned long long* tile_counter;    // zeroed before the launch
+};
+
 struct BStepParams {
+    Fwd2Params fwd2;  // fwd2.layer_done == nullptr: not fused
     int m1, n1;
     long long ncol;  // columns per pair
     long long ncell, nface;

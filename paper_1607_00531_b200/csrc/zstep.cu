@@ -27,6 +27,9 @@ namespace {
 #ifndef EPC_GEMM_BK
 #define EPC_GEMM_BK 16  // k-slab depth; 32 measured slower for three of the four transforms
 #endif
+#ifndef EPC_GEMM_DB
+#define EPC_GEMM_DB 1
+#endif
 #ifndef EPC_GEMM_MFIRST
 #define EPC_GEMM_MFIRST 1
 #endif
@@ -42,8 +45,13 @@ template <int PRO, int EPI, int RM>
 // registers (measured), the other variants fit three CTAs unforced.
 __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmParams p) {
     constexpr int BM = 16 * RM;
-    __shared__ double As[BK][BM + 1];  // +1: the transposing store is conflict-free
-    __shared__ double Bs[BK][BN];
+    // DB: two K-slab buffers, one barrier per slab (the next slab is stored
+    // into the other buffer while this one is read). Measured per transform
+    // (scripts/r02db_gpu.sh): the dual GEMM (three CTAs per SM) 0.309 ->
+    // 0.287 ms; the others (two CTAs per SM) 1-2% slower, so single-buffered
+    constexpr bool DB = EPC_GEMM_DB && EPI == EPI_DUAL;
+    __shared__ double As[DB ? 2 : 1][BK][BM + 1];  // +1: the transposing store is conflict-free
+    __shared__ double Bs[DB ? 2 : 1][BK][BN];
     __shared__ double red[(NT / 32) * 6];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     // M tiles innermost in launch order: the CTAs sharing one B (column)
@@ -93,24 +101,21 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
         }
     };
 
-    load_tile(0);
-    for (int k0 = 0; k0 < p.K; k0 += BK) {
-        __syncthreads();
+    auto store_tile = [&](int buf) {
 #pragma unroll
-        for (int t = 0; t < NA; ++t) As[ak][am + AR * t] = ra[t];
+        for (int t = 0; t < NA; ++t) As[buf][ak][am + AR * t] = ra[t];
 #pragma unroll
-        for (int t = 0; t < NB; ++t) Bs[lk + 4 * t][ln] = rb[t];
-        __syncthreads();
-        if (k0 + BK < p.K) load_tile(k0 + BK);
-        const int kend = min(BK, p.K - k0);
+        for (int t = 0; t < NB; ++t) Bs[buf][lk + 4 * t][ln] = rb[t];
+    };
+    auto mac_slab = [&](int buf, int kend) {
         if (kend == BK) {
 #pragma unroll
             for (int kk = 0; kk < BK; ++kk) {
                 double a[RM], b[4];
 #pragma unroll
-                for (int r = 0; r < RM; ++r) a[r] = As[kk][ty + 16 * r];
+                for (int r = 0; r < RM; ++r) a[r] = As[buf][kk][ty + 16 * r];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
+                for (int c = 0; c < 4; ++c) b[c] = Bs[buf][kk][tx + 16 * c];
 #pragma unroll
                 for (int r = 0; r < RM; ++r)
 #pragma unroll
@@ -120,14 +125,37 @@ __global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmPa
             for (int kk = 0; kk < kend; ++kk) {
                 double a[RM], b[4];
 #pragma unroll
-                for (int r = 0; r < RM; ++r) a[r] = As[kk][ty + 16 * r];
+                for (int r = 0; r < RM; ++r) a[r] = As[buf][kk][ty + 16 * r];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
+                for (int c = 0; c < 4; ++c) b[c] = Bs[buf][kk][tx + 16 * c];
 #pragma unroll
                 for (int r = 0; r < RM; ++r)
 #pragma unroll
                     for (int c = 0; c < 4; ++c) acc[r][c] = acc[r][c] + a[r] * b[c];
             }
+        }
+    };
+
+    load_tile(0);
+    if constexpr (DB) {
+        store_tile(0);
+        __syncthreads();
+        int buf = 0;
+        for (int k0 = 0; k0 < p.K; k0 += BK) {
+            const bool more = k0 + BK < p.K;
+            if (more) load_tile(k0 + BK);
+            mac_slab(buf, min(BK, p.K - k0));
+            if (more) store_tile(buf ^ 1);  // last read at the previous slab, behind its barrier
+            __syncthreads();
+            buf ^= 1;
+        }
+    } else {
+        for (int k0 = 0; k0 < p.K; k0 += BK) {
+            __syncthreads();
+            store_tile(0);
+            __syncthreads();
+            if (k0 + BK < p.K) load_tile(k0 + BK);
+            mac_slab(0, min(BK, p.K - k0));
         }
     }
 
