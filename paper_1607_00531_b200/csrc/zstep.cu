@@ -27,6 +27,9 @@ namespace {
 #ifndef EPC_GEMM_BK
 #define EPC_GEMM_BK 16  // k-slab depth; 32 measured slower for three of the four transforms
 #endif
+#ifndef EPC_GEMM_MINB
+#define EPC_GEMM_MINB 1  // resident CTAs per SM asked of the RM = 4 non-dual GEMMs (3: forward axis 2 0.287 -> 0.296 ms, scripts/r02mb_gpu.sh)
+#endif
 #ifndef EPC_GEMM_DB
 #define EPC_GEMM_DB 1
 #endif
@@ -43,7 +46,7 @@ template <int PRO, int EPI, int RM>
 // The dual epilogue needs more registers than the plain ones; capping it to
 // three resident CTAs per SM (<= 85 registers) is faster than two with more
 // registers (measured), the other variants fit three CTAs unforced.
-__global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : 1) k_dct_gemm(GemmParams p) {
+__global__ void __launch_bounds__(NT, EPI == EPI_DUAL ? 3 : (RM == 4 ? EPC_GEMM_MINB : 1)) k_dct_gemm(GemmParams p) {
     constexpr int BM = 16 * RM;
     // DB: two K-slab buffers, one barrier per slab (the next slab is stored
     // into the other buffer while this one is read). Measured per transform

@@ -107,20 +107,22 @@ def test_gn_c3_vs_reference(ctx):
     assert sum(x["pcg_iters"] for x in r["rows"]) > 100
 
 
-def test_admm_batch_pairs_each_bitwise(ctx, oracle):
+@pytest.mark.parametrize("m", [(16, 12, 8), (128, 8, 6)])
+def test_admm_batch_pairs_each_bitwise(ctx, oracle, m):
     """epc_admm_solve_batch (C4's entry point) with pairs that stop at
     different iterations under the default tolerances, pairs at different
     intensity scales (x1, x400, x20) and one pair whose column 5 fails
     (a NaN intensity: 'column factor: nonpositive pivot' at iteration 1):
     each pair bitwise against its own admm_solve (admm.cpp:488-560), the
-    failed pair's state the one from before the failed iteration."""
-    m = (16, 12, 8)
+    failed pair's state the one from before the failed iteration.
+    At n1 = 129 the forward axis-2 DCT runs in the b-step's drain (layer
+    counts over skipped columns of stopped pairs and failing columns)."""
     g, ip, im = synth.make_batch("C4", npairs=3, m=m)
     nc, nf = g.cells, g.faces
     ips = [ip[q * nc:(q + 1) * nc].copy() for q in range(3)]
     ims = [im[q * nc:(q + 1) * nc].copy() for q in range(3)]
     bad = ips[0].copy()
-    bad[16 * 5 + 3] = np.nan
+    bad[m[0] * 5 + 3] = np.nan
     ips += [ips[0] * 400.0, bad, ips[1] * 20.0]
     ims += [ims[0] * 400.0, ims[0].copy(), ims[1] * 20.0]
     P = len(ips)
