@@ -71,7 +71,7 @@ def parse():
 
 # fp64 DADD/DMUL issue rate measured on this pool (profiles/r01_ubench_fp64_tput.log)
 FP64_PEAK_TOPS = 18.3
-NCU_BSTEP_SUMMARY = "r02fz_bstep_c3_late_ncu.json"  # C3 b-step, launch 91 of 100, ncu --set full
+NCU_BSTEP_SUMMARY = "r02ff_bstep_c3_late_ncu.json"  # C3 b-step, launch 91 of 100, ncu --set full
 # the GN-PCG kernels' ncu captures: C2 runs the persistent loop (L2-resident),
 # C3 the per-iteration kernels (k_pcg_hvp, k_pcg_update_bj)
 NCU_PCG_SUMMARY = {"C2": "r02fin_pcg_c2_ncu.json", "C3": "r02fin_pcg_parts_c3_ncu.json"}
