@@ -103,7 +103,7 @@ enum Slot {
     S_ML0, S_ML1, S_MLI, S_MLD, S_MLB, S_MLO, S_MLIP, S_MLIM, S_MLFIP, S_MLFIM,
     S_F32_IP, S_F32_IM, S_F32_B0, S_F32_B1, S_F32_Z0, S_F32_Z1, S_F32_U0, S_F32_U1, S_F32_T0,
     S_F32_T1, S_F32_MATS, S_F32_Q, S_F32_S, S_F32_COL, S_F32_SCAL, S_F32_PART,
-    S_CTIME, S_SEQ, S_ACTL, S_FUSE,
+    S_CTIME, S_SEQ, S_ACTL, S_FUSE, S_LPTC, S_LPTO,
     S_SN0, S_SN1, S_SN2, S_SN3, S_SN4, S_SN5, S_SN6, S_SN7, S_SN8, S_SN9, S_SNH, S_SNG,
     S_COUNT
 };
@@ -375,7 +375,8 @@ struct BStepRun {
 BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip, const double* im,
                    const double* b, const double* z, const double* u, double* b_out,
                    const double* rho_dev, const int* active_dev, double alpha,
-                   const epc_admm_config* cfg, const Fwd2Params* fwd2 = nullptr) {
+                   const epc_admm_config* cfg, const Fwd2Params* fwd2 = nullptr,
+                   unsigned* col_cost = nullptr, const int* order = nullptr) {
     const long long total = g.ncol * npairs;
     const HDiv hd = make_hdiv(g.h1);
     // EPC_BSTEP_TAIL (dev aid): per-CTA exit times and per-column durations,
@@ -465,6 +466,8 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
         P.fwd2.tile_counter = fc;
         P.fwd2.layer_done = reinterpret_cast<unsigned*>(fc + 1);
     }
+    P.col_cost = col_cost;
+    P.order = order;
     if (tail && total < (1LL << 31)) P.col_ns = slot_t<unsigned>(ctx, S_CTIME, (size_t)total);
     P.cta_span = tail ? slot_t<unsigned long long>(ctx, S_GN8, (size_t)slots * 2) : nullptr;
     static const char* dump = getenv("EPC_BSTEP_DUMP");  // dev aid: per-column records
@@ -1035,6 +1038,25 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
         static const double fuse_max_ms = getenv("EPC_FUSE_MAX_MS") ? atof(getenv("EPC_FUSE_MAX_MS")) : 12.0;
         const bool fuse_fwd2_ok = fuse_env && g.m3 > 1;
         double prev_bstep_ms = -1.0;  // the previous iteration's b-step (events eb0 / eb1)
+        // Longest columns first while the launches are bulk-bound (the first
+        // ~25 iterations of a C3 solve: 5-12 ms launches whose column costs
+        // repeat from one iteration to the next, correlation 0.9-0.98, and
+        // whose last 11-15% is an under-filled tail): every launch records
+        // its columns' cycles, and after a launch of EPC_LPT_MIN_MS or more the
+        // next one claims columns by descending recorded cost. Late launches'
+        // heavy columns do not repeat (DESIGN 4), so they keep the k-layer
+        // order, which also feeds the fused forward axis-2 transform early.
+        // Columns are independent: the order cannot change a bit of b.
+        static const double lpt_min_ms = getenv("EPC_LPT_MIN_MS") ? atof(getenv("EPC_LPT_MIN_MS")) : 5.0;
+        const long long total_cols = g.ncol * npairs;
+        const bool lpt_ok = total_cols < (1LL << 31);
+        // two cost arrays, written alternately. EPC_LPT_TWO=1 keys the order on
+        // the larger of the last two launches' costs (measured: no better than
+        // the last launch's alone, profiles/r02fj_lpt_ab.log; off by default)
+        static const bool lpt_two = getenv("EPC_LPT_TWO") && atoi(getenv("EPC_LPT_TWO")) != 0;
+        unsigned* lpt_cost = lpt_ok ? slot_t<unsigned>(ctx, S_LPTC, (size_t)total_cols * 2) : nullptr;
+        int lpt_have = 0;  // launches of this solve that recorded their costs
+        int* lpt_order = lpt_ok ? slot_t<int>(ctx, S_LPTO, (size_t)total_cols) : nullptr;
         for (int it = 1; !device_loop && it <= cfg->max_iter && n_active > 0; ++it) {
             // ---- b-step ----------------------------------------------------------
             CK(cudaEventRecord(eb0, ctx->stream));
@@ -1053,9 +1075,17 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
                 f2.m3 = g.m3;
                 f2.npairs = npairs;
             }
+            const bool lpt = lpt_ok && prev_bstep_ms >= lpt_min_ms;
+            unsigned* cost_now = lpt_ok ? lpt_cost + (size_t)(lpt_have & 1) * total_cols : nullptr;
+            if (lpt) {
+                const unsigned* c1 = lpt_cost + (size_t)((lpt_have - 1) & 1) * total_cols;
+                const unsigned* c2 = (lpt_have >= 2 && lpt_two) ? cost_now : c1;  // two launches ago
+                EPC_LAUNCH(ctx, "lpt_order", k_lpt_order, 1, 1024, 0, c1, c2, lpt_order, total_cols);
+            }
             BStepRun br = run_bstep(ctx, g, npairs, ip, im, B[0], Z[0], U[0], B[1], rho_dev,
                                     batch ? act_dev : nullptr, p->alpha, cfg,
-                                    fuse_fwd2 ? &f2 : nullptr);
+                                    fuse_fwd2 ? &f2 : nullptr, cost_now, lpt ? lpt_order : nullptr);
+            ++lpt_have;
             CK(cudaEventRecord(eb1, ctx->stream));
             const long long total = g.ncol * npairs;
             EPC_LAUNCH(ctx, "reduce_columns", k_reduce_columns, npairs, 1024, 0, br.col_i,

@@ -47,7 +47,14 @@ struct BStepParams {
     unsigned long long* cta_span;  // optional [2 x grid]: %globaltimer at CTA start / exit (dev aid)
     unsigned* col_ns;   // optional: each column's duration in ns (dev aid, EPC_BSTEP_TAIL)
     float* col_sn;      // optional [2 x total]: step norms of SQP iterations 0, 1 (dev aid)
+    // longest-columns-first scheduling (api.cu: the early, bulk-bound launches):
+    unsigned* col_cost;  // optional [total]: each column's cycles / 16, for the next launch's order
+    const int* order;    // optional [total]: the queue's n-th claim runs column order[n]
 };
+// columns by descending cost, the larger of the last two launches' (256 linear
+// buckets, unordered within a bucket: columns are independent, any order
+// gives the same bits)
+__global__ void k_lpt_order(const unsigned* cost, const unsigned* cost2, int* order, long long total);
 // DH = HPow2 | HGen (model.cuh); DIAG: phase timing / counters and the
 // chained mode compiled in (diagnostic instantiation, selected by ctx->mode)
 // IMG: I+/I- read from global memory through L1 instead of staged in shared
