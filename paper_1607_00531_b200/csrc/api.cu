@@ -103,7 +103,7 @@ enum Slot {
     S_ML0, S_ML1, S_MLI, S_MLD, S_MLB, S_MLO, S_MLIP, S_MLIM, S_MLFIP, S_MLFIM,
     S_F32_IP, S_F32_IM, S_F32_B0, S_F32_B1, S_F32_Z0, S_F32_Z1, S_F32_U0, S_F32_U1, S_F32_T0,
     S_F32_T1, S_F32_MATS, S_F32_Q, S_F32_S, S_F32_COL, S_F32_SCAL, S_F32_PART,
-    S_CTIME, S_SEQ, S_ACTL, S_FUSE, S_LPTC, S_LPTO,
+    S_CTIME, S_SEQ, S_ACTL, S_FUSE, S_LPTC, S_LPTO, S_LPTK,
     S_SN0, S_SN1, S_SN2, S_SN3, S_SN4, S_SN5, S_SN6, S_SN7, S_SN8, S_SN9, S_SNH, S_SNG,
     S_COUNT
 };
@@ -376,7 +376,7 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
                    const double* b, const double* z, const double* u, double* b_out,
                    const double* rho_dev, const int* active_dev, double alpha,
                    const epc_admm_config* cfg, const Fwd2Params* fwd2 = nullptr,
-                   unsigned* col_cost = nullptr, const int* order = nullptr) {
+                   unsigned* col_cost = nullptr, const int* order = nullptr, unsigned* crit = nullptr) {
     const long long total = g.ncol * npairs;
     const HDiv hd = make_hdiv(g.h1);
     // EPC_BSTEP_TAIL (dev aid): per-CTA exit times and per-column durations,
@@ -468,6 +468,7 @@ BStepRun run_bstep(epc_context* ctx, const Geo& g, int npairs, const double* ip,
     }
     P.col_cost = col_cost;
     P.order = order;
+    P.crit = order ? crit : nullptr;
     if (tail && total < (1LL << 31)) P.col_ns = slot_t<unsigned>(ctx, S_CTIME, (size_t)total);
     P.cta_span = tail ? slot_t<unsigned long long>(ctx, S_GN8, (size_t)slots * 2) : nullptr;
     static const char* dump = getenv("EPC_BSTEP_DUMP");  // dev aid: per-column records
@@ -1056,6 +1057,16 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
         static const bool lpt_two = getenv("EPC_LPT_TWO") && atoi(getenv("EPC_LPT_TWO")) != 0;
         unsigned* lpt_cost = lpt_ok ? slot_t<unsigned>(ctx, S_LPTC, (size_t)total_cols * 2) : nullptr;
         int lpt_have = 0;  // launches of this solve that recorded their costs
+        // A column predicted to outlast the balanced makespan (its cost at least
+        // EPC_LPT_CRIT, default 0.8, of total / resident warps; x400: a handful
+        // of 50-75 ms columns against 45 ms) bounds the launch by itself, and
+        // runs 20-40% slower beside seven other heavy columns than alone. While
+        // one runs, its SM's other warps wait instead of claiming (at most 32
+        // such columns per launch; none at unit intensity).
+        static const double lpt_crit = getenv("EPC_LPT_CRIT") ? atof(getenv("EPC_LPT_CRIT")) : 0.8;
+        const int nsm_pad = 1024;  // %smid < this on any part
+        unsigned* lpt_critbuf = (lpt_ok && lpt_crit > 0.0) ? slot_t<unsigned>(ctx, S_LPTK, 1 + nsm_pad) : nullptr;
+        const double lpt_slots = (double)std::min<long long>((long long)ctx->num_sms * 8, total_cols);
         int* lpt_order = lpt_ok ? slot_t<int>(ctx, S_LPTO, (size_t)total_cols) : nullptr;
         for (int it = 1; !device_loop && it <= cfg->max_iter && n_active > 0; ++it) {
             // ---- b-step ----------------------------------------------------------
@@ -1080,11 +1091,12 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
             if (lpt) {
                 const unsigned* c1 = lpt_cost + (size_t)((lpt_have - 1) & 1) * total_cols;
                 const unsigned* c2 = (lpt_have >= 2 && lpt_two) ? cost_now : c1;  // two launches ago
-                EPC_LAUNCH(ctx, "lpt_order", k_lpt_order, 1, 1024, 0, c1, c2, lpt_order, total_cols);
+                EPC_LAUNCH(ctx, "lpt_order", k_lpt_order, 1, 1024, 0, c1, c2, lpt_order, total_cols,
+                           lpt_critbuf, lpt_crit / lpt_slots, 32, nsm_pad);
             }
             BStepRun br = run_bstep(ctx, g, npairs, ip, im, B[0], Z[0], U[0], B[1], rho_dev,
                                     batch ? act_dev : nullptr, p->alpha, cfg,
-                                    fuse_fwd2 ? &f2 : nullptr, cost_now, lpt ? lpt_order : nullptr);
+                                    fuse_fwd2 ? &f2 : nullptr, cost_now, lpt ? lpt_order : nullptr, lpt_critbuf);
             ++lpt_have;
             CK(cudaEventRecord(eb1, ctx->stream));
             const long long total = g.ncol * npairs;

@@ -50,11 +50,16 @@ struct BStepParams {
     // longest-columns-first scheduling (api.cu: the early, bulk-bound launches):
     unsigned* col_cost;  // optional [total]: each column's cycles / 16, for the next launch's order
     const int* order;    // optional [total]: the queue's n-th claim runs column order[n]
+    // with order: crit[0] = n, the first n claims are columns predicted to outlast
+    // the balanced makespan; crit[1 + smid] counts those running on an SM, whose
+    // other warps wait instead of claiming (0 / nullptr: no reservation)
+    unsigned* crit;
 };
 // columns by descending cost, the larger of the last two launches' (256 linear
 // buckets, unordered within a bucket: columns are independent, any order
 // gives the same bits)
-__global__ void k_lpt_order(const unsigned* cost, const unsigned* cost2, int* order, long long total);
+__global__ void k_lpt_order(const unsigned* cost, const unsigned* cost2, int* order, long long total,
+                            unsigned* crit, double crit_share, int max_crit, int nsm);
 // DH = HPow2 | HGen (model.cuh); DIAG: phase timing / counters and the
 // chained mode compiled in (diagnostic instantiation, selected by ctx->mode)
 // IMG: I+/I- read from global memory through L1 instead of staged in shared
