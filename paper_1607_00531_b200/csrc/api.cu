@@ -1063,9 +1063,13 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
         // runs 20-40% slower beside seven other heavy columns than alone. While
         // one runs, its SM's other warps wait instead of claiming (at most 32
         // such columns per launch; none at unit intensity).
+#ifdef EPC_CRIT
         static const double lpt_crit = getenv("EPC_LPT_CRIT") ? atof(getenv("EPC_LPT_CRIT")) : 0.8;
+#else  // the kernel side is compiled out by default (it costs 0.8% at unit intensity)
+        static const double lpt_crit = 0.0;
+#endif
         const int nsm_pad = 1024;  // %smid < this on any part
-        unsigned* lpt_critbuf = (lpt_ok && lpt_crit > 0.0) ? slot_t<unsigned>(ctx, S_LPTK, 1 + nsm_pad) : nullptr;
+        unsigned* lpt_critbuf = (lpt_ok && lpt_crit > 0.0) ? slot_t<unsigned>(ctx, S_LPTK, 1 + nsm_pad + 4096) : nullptr;  // + a flag per CTA
         const double lpt_slots = (double)std::min<long long>((long long)ctx->num_sms * 8, total_cols);
         int* lpt_order = lpt_ok ? slot_t<int>(ctx, S_LPTO, (size_t)total_cols) : nullptr;
         for (int it = 1; !device_loop && it <= cfg->max_iter && n_active > 0; ++it) {
@@ -1092,7 +1096,7 @@ int admm_solve_impl(epc_context* ctx, const epc_grid* gg, int npairs, int mem, c
                 const unsigned* c1 = lpt_cost + (size_t)((lpt_have - 1) & 1) * total_cols;
                 const unsigned* c2 = (lpt_have >= 2 && lpt_two) ? cost_now : c1;  // two launches ago
                 EPC_LAUNCH(ctx, "lpt_order", k_lpt_order, 1, 1024, 0, c1, c2, lpt_order, total_cols,
-                           lpt_critbuf, lpt_crit / lpt_slots, 32, nsm_pad);
+                           lpt_critbuf, lpt_crit / lpt_slots, 32, nsm_pad + 4096);
             }
             BStepRun br = run_bstep(ctx, g, npairs, ip, im, B[0], Z[0], U[0], B[1], rho_dev,
                                     batch ? act_dev : nullptr, p->alpha, cfg,
